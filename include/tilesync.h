@@ -1,0 +1,187 @@
+/*
+ * tilesync.h — C ABI of libtilesync_b200.so, the B200 (sm_100a) implementation of
+ * tile-level semaphore synchronization between dependent kernels (arXiv 2305.13450,
+ * "CuSync").
+ *
+ * The reference (/root/reference) ships no native code: its hot-path API is the Python
+ * policy layer `tilesync_sim.policies` plus the CUDA listings of the paper. Each entry
+ * point below names the reference interface it replaces.
+ *
+ * Conventions
+ *   - Plain C types only. Device pointers are `void*`/`int*`; streams are `void*`
+ *     (a cudaStream_t, 0 = legacy default stream).
+ *   - Every function returns a ts_status. On failure `ts_last_error()` returns a
+ *     thread-local message. Status codes map onto the reference's exception types
+ *     (/root/reference/pkg/src/tilesync_sim/errors.py:4-9, policies.py:102-112,
+ *     gpu.py:63-67): TS_ERR_CONFIG -> ConfigError, TS_ERR_VALUE -> ValueError,
+ *     TS_ERR_TYPE -> TypeError.
+ *   - The library allocates no persistent device memory. The caller (PyTorch) owns
+ *     every buffer; the library borrows pointers for the duration of one
+ *     stream-ordered call.
+ *   - Host functions are reentrant. One in-flight chain per semaphore array.
+ */
+#ifndef TILESYNC_B200_H
+#define TILESYNC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_ABI_VERSION 1
+
+/* ---- status codes ---------------------------------------------------------------- */
+typedef enum {
+  TS_OK = 0,
+  TS_ERR_CONFIG = 1,   /* ConfigError  (errors.py:4-5)                     */
+  TS_ERR_VALUE = 2,    /* ValueError   (gpu.py:63-67, policies.py:133,188) */
+  TS_ERR_TYPE = 3,     /* TypeError    (policies.py:125,142,166,178,205)   */
+  TS_ERR_CUDA = 4,     /* CUDA runtime/driver failure                      */
+  TS_ERR_DEADLOCK = 5  /* device watchdog fired (engine.py:614-637)        */
+} ts_status;
+
+/* ---- policy and order kinds (policies.py:24-73) ---------------------------------- */
+typedef enum {
+  TS_POLICY_TILE = 0,    /* TileSync       policies.py:24-26 */
+  TS_POLICY_ROW = 1,     /* RowSync        policies.py:29-31 */
+  TS_POLICY_STRIDED = 2, /* StridedSync    policies.py:34-38, param = stride */
+  TS_POLICY_CONV2D = 3   /* Conv2DTileSync policies.py:41-50, param = kk     */
+} ts_policy_kind;
+
+typedef enum {
+  TS_ORDER_ROW_MAJOR = 0,        /* RowMajor        policies.py:56-58 */
+  TS_ORDER_STRIDED_ROW_MAJOR = 1 /* StridedRowMajor policies.py:61-70, param = stride */
+} ts_order_kind;
+
+/* ---- host mirrors of the policy layer --------------------------------------------
+ * These run the exact __host__ __device__ functions the kernels use, so the Python
+ * drop-in and the device agree by construction. */
+
+/* ABI version (TS_ABI_VERSION). */
+int ts_abi_version(void);
+
+/* Thread-local message for the last non-OK status. */
+const char* ts_last_error(void);
+
+/* sem_count(policy, producer_grid) — policies.py:115-125 (+check_policy 102-112). */
+int ts_sem_count(int policy, int param, int gx, int gy, int gz, int* out);
+
+/* post_target(policy, tile, producer_grid) — policies.py:128-142. */
+int ts_post_target(int policy, int param, int tx, int ty, int tz, int gx, int gy,
+                   int gz, int* out);
+
+/* consumer_wait(policy, consumer_tile, k_step, producer_grid, producer_z)
+ * — policies.py:145-166. *sem = -1 encodes `None`. */
+int ts_consumer_wait(int policy, int param, int tx, int ty, int tz, int k_step, int pgx,
+                     int pgy, int pgz, int producer_z, int* sem, int* expected);
+
+/* wait_steps(policy, k_steps) — policies.py:169-178. Writes up to `cap` steps. */
+int ts_wait_steps(int policy, int param, int k_steps, int* out, int cap, int* n);
+
+/* order_tile(order, grid, counter) — policies.py:181-205. */
+int ts_order_tile(int order, int stride, int gx, int gy, int gz, int counter, int* x,
+                  int* y, int* z);
+
+/* avoid_wait_kernel(producer, consumer, gpu) — engine.py:173-180 ("+W"). */
+int ts_avoid_wait_kernel(int prod_tiles, int prod_occ, int cons_tiles, int cons_occ,
+                         int num_sms, int* out);
+
+/* ---- chain launch ------------------------------------------------------------------
+ * A chain is a list of tile stages (GeMM kernels C = epi(A x B^T)) plus dependency
+ * edges. It replaces the paper's CuSync/CuStage host code and the
+ * reference's Scenario (engine.py:71-131). */
+
+#define TS_MAX_STAGES 4
+#define TS_MAX_DEPS 4
+
+typedef enum { TS_DTYPE_F16 = 0, TS_DTYPE_BF16 = 1 } ts_dtype;
+
+typedef enum {
+  TS_EPI_NONE = 0,   /* C = A x B^T                                        */
+  TS_EPI_GELU = 1,   /* C = GeLU_erf(A x B^T)   */
+  TS_EPI_SWIGLU = 2  /* C = SiLU(gate) * up, gate/up interleaved per tile  */
+} ts_epilogue;
+
+typedef enum {
+  TS_MODE_STREAM = 0, /* one launch per stage on one stream, no semaphores (baseline) */
+  TS_MODE_FUSED = 1   /* one persistent launch over all stages' tiles, semaphores     */
+} ts_mode;
+
+typedef enum {
+  TS_FLAG_KEEP_SEMS = 1,   /* do not zero semaphores at exit (for final-value parity)  */
+  TS_FLAG_NO_REORDER = 2,  /* disable "+R": load the dependent A tile before B         */
+  TS_FLAG_NO_WATCHDOG = 4  /* spin forever instead of aborting a wait after ~4 s      */
+} ts_flags;
+
+typedef struct {
+  const void* a; /* [m, k] row-major, lda elements                         */
+  const void* b; /* [n, k] row-major (weights, K-major), ldb elements      */
+  void* c;       /* [m, n_out] row-major, ldc elements                     */
+  int m, n, k;   /* n = accumulator columns (for SwiGLU n_out = n / 2)      */
+  int lda, ldb, ldc;
+  int dtype;     /* ts_dtype  */
+  int epilogue;  /* ts_epilogue */
+  int order;     /* ts_order_kind */
+  int order_stride;
+} ts_stage_desc;
+
+typedef struct {
+  int producer, consumer; /* stage indices, producer < consumer                 */
+  int operand;            /* 0 = consumer's A operand (the only one GeMMs read) */
+  int policy, param;      /* ts_policy_kind + stride / kk                        */
+  int* sem;               /* device int32[sem_count], zero on entry             */
+} ts_dep_desc;
+
+typedef struct {
+  int n_stages;
+  ts_stage_desc stages[TS_MAX_STAGES];
+  int n_deps;
+  ts_dep_desc deps[TS_MAX_DEPS];
+  int mode;      /* ts_mode */
+  int tile_n;    /* 64, 128 or 256; 0 = 256 */
+  int flags;     /* ts_flags bitmask */
+  int num_ctas;  /* persistent CTAs; 0 = one per SM */
+  int* scratch;  /* device int32[TS_SCRATCH_INTS], zero on first use; kernels restore it */
+  void* trace;   /* optional device ts_trace_rec[trace_cap]; NULL = no tracing */
+  int trace_cap;
+} ts_chain_desc;
+
+#define TS_SCRATCH_INTS 8
+/* scratch layout: [0] work counter, [1] CTA exit counter, [2] trace count,
+ *                 [3] watchdog flag (1 = a wait timed out), [4..7] reserved */
+
+/* Device trace record (one event of the reference's JSONL schema, engine.py:220-248). */
+typedef struct {
+  uint64_t t_ns;     /* %globaltimer */
+  int32_t kind;      /* 0 scheduled, 1 wait_begin, 2 wait_end, 3 post, 4 finished */
+  int32_t stage;     /* stage index */
+  int32_t tb;        /* claim index within the stage (reference `tb`) */
+  int32_t k;         /* reference k-step, -1 = none */
+  int32_t dep;       /* dependency index, -1 = none */
+  int32_t sem;       /* semaphore index, -1 = none */
+  int32_t value;     /* expected (wait_*) or post value (post), -1 = none */
+  int16_t x, y;      /* tile coordinate */
+  int16_t z, smid;   /* slice, SM id */
+  int32_t pad;
+} ts_trace_rec;
+
+/* Validate `desc` on the host and enqueue the chain on `stream`. Returns before the
+ * device work completes. */
+int ts_chain_launch(const ts_chain_desc* desc, void* stream);
+
+/* Number of work items (tiles) a fused launch of `desc` processes, and the tile grid
+ * of stage `s` (rows x cols) as the reference Stage.grid sees it. */
+int ts_chain_grid(const ts_chain_desc* desc, int s, int* gx, int* gy);
+
+/* Paper's wait kernel: one thread on `stream` spins until every
+ * flags[i] != 0 (each set by the producer's stage.start()). */
+int ts_wait_kernel_launch(const int* flags, int n, void* stream);
+
+/* SM count of the current device. */
+int ts_device_sm_count(int* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TILESYNC_B200_H */

@@ -1,0 +1,78 @@
+"""The paper's dependent-kernel chains as ready-made CuSync builders.
+
+* GPT-3 MLP: ``XW1 = GeLU(X @ W1)``, ``XW12 = XW1 @ W2`` — two
+  dependent GeMMs, RowSync or TileSync.
+* LLaMA-style SwiGLU MLP (BASELINE.json configs[3]): ``H = SiLU(X Wg) * (X Wu)``,
+  ``Y = H Wd`` with gate/up columns interleaved per tile so one tile's accumulator holds
+  matching gate and up columns (``interleave_gate_up``).
+
+Weights are stored K-major, i.e. ``W1`` as ``[N, K]`` (nn.Linear layout): the chain
+computes ``A @ W^T``.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .cusync import CuSync
+from .policies import RowSync, SyncPolicy
+
+
+class MlpChain:
+    """GeMM -> GeLU -> GeMM with a reusable CuSync (semaphores, scratch, descriptor)."""
+
+    def __init__(self, x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor,
+                 policy: SyncPolicy = RowSync(), mode: str = "fused", tile_n: int = 256,
+                 reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0):
+        m = x.shape[0]
+        self.x, self.w1, self.w2 = x, w1, w2
+        self.h = torch.empty(m, w1.shape[0], dtype=x.dtype, device=x.device)
+        self.y = torch.empty(m, w2.shape[0], dtype=x.dtype, device=x.device)
+        self.cs = CuSync(tile_n=tile_n, mode=mode, reorder=reorder, keep_sems=keep_sems,
+                         num_ctas=num_ctas)
+        self.prod = self.cs.stage(x, w1, self.h, epilogue="gelu", id="gemm1")
+        self.cons = self.cs.stage(self.h, w2, self.y, id="gemm2")
+        self.dep = self.cs.dependency(policy, self.prod, self.cons, operand="a")
+
+    def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        self.cs.launch(stream)
+        return self.y
+
+
+def mlp(x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor, policy: SyncPolicy = RowSync(),
+        mode: str = "fused", tile_n: int = 256) -> torch.Tensor:
+    """One-shot GPT-3 MLP: ``GeLU(x @ w1^T) @ w2^T`` on the B200 chain kernel."""
+    return MlpChain(x, w1, w2, policy, mode, tile_n)()
+
+
+def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor, tile_n: int) -> torch.Tensor:
+    """Pack [F, K] gate and up weights into [2F, K] so every tile_n-row block holds
+    tile_n/2 gate rows followed by the matching tile_n/2 up rows."""
+    f, k = w_gate.shape
+    half = tile_n // 2
+    if f % half:
+        raise ValueError(f"F={f} must be a multiple of tile_n/2={half}")
+    g = w_gate.reshape(f // half, half, k)
+    u = w_up.reshape(f // half, half, k)
+    return torch.cat([g, u], dim=1).reshape(2 * f, k).contiguous()
+
+
+class SwigluChain:
+    """GeMM(gate|up) -> SwiGLU -> GeMM(down)."""
+
+    def __init__(self, x: torch.Tensor, w_gate_up: torch.Tensor, w_down: torch.Tensor,
+                 policy: SyncPolicy = RowSync(), mode: str = "fused", tile_n: int = 256,
+                 reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0):
+        m = x.shape[0]
+        f = w_gate_up.shape[0] // 2
+        self.h = torch.empty(m, f, dtype=x.dtype, device=x.device)
+        self.y = torch.empty(m, w_down.shape[0], dtype=x.dtype, device=x.device)
+        self.cs = CuSync(tile_n=tile_n, mode=mode, reorder=reorder, keep_sems=keep_sems,
+                         num_ctas=num_ctas)
+        self.prod = self.cs.stage(x, w_gate_up, self.h, epilogue="swiglu", id="gate_up")
+        self.cons = self.cs.stage(self.h, w_down, self.y, id="down")
+        self.dep = self.cs.dependency(policy, self.prod, self.cons, operand="a")
+
+    def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        self.cs.launch(stream)
+        return self.y

@@ -1,0 +1,401 @@
+// ts_abi.cu — the extern "C" boundary of libtilesync_b200.so (declared in
+// include/tilesync.h). Host-side validation mirrors the reference's structural checks
+// (validate_scenario, /root/reference/pkg/src/tilesync_sim/engine.py:134-170; check_policy,
+// policies.py:102-112) so errors surface as the same exception types before any launch.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "tilesync.h"
+#include "ts_chain_kernel.cuh"
+#include "ts_policy.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(TS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// K-major [rows, k] 16-bit matrix, leading dimension `ld` elements, box {64, box_rows}.
+int make_tmap(CUtensorMap* m, const void* ptr, int rows, int k, int ld, int dtype,
+              int box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(TS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(ts::kBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, dtype == TS_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%d k=%d ld=%d", (int)r,
+                rows, k, ld);
+  return TS_OK;
+}
+
+int sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return n;
+}
+
+template <int BN, typename T>
+int launch_one(const ts::ChainParams& p, int grid, cudaStream_t stream) {
+  using C = ts::Cfg<BN>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(ts::chain_kernel<BN, T>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
+  ts::chain_kernel<BN, T><<<grid, ts::kThreads, C::kSmemBytes, stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "chain_kernel launch");
+  return TS_OK;
+}
+
+int launch_dispatch(int bn, int dtype, const ts::ChainParams& p, int grid, cudaStream_t s) {
+  if (dtype == TS_DTYPE_BF16) {
+    switch (bn) {
+      case 64: return launch_one<64, __nv_bfloat16>(p, grid, s);
+      case 128: return launch_one<128, __nv_bfloat16>(p, grid, s);
+      case 256: return launch_one<256, __nv_bfloat16>(p, grid, s);
+    }
+  } else {
+    switch (bn) {
+      case 64: return launch_one<64, __half>(p, grid, s);
+      case 128: return launch_one<128, __half>(p, grid, s);
+      case 256: return launch_one<256, __half>(p, grid, s);
+    }
+  }
+  return fail(TS_ERR_VALUE, "tile_n must be 64, 128 or 256 (got %d)", bn);
+}
+
+int tile_n_of(const ts_chain_desc* d) { return d->tile_n == 0 ? 256 : d->tile_n; }
+
+// Output columns one tile of stage `st` writes (the producer "column tile" width that a
+// consumer k-step covers).
+int out_tile_cols(const ts_stage_desc& st, int bn) {
+  return st.epilogue == TS_EPI_SWIGLU ? bn / 2 : bn;
+}
+
+// Validate the descriptor and fill kernel parameters (everything but tensor maps when
+// `with_tmaps` is false, so ts_chain_grid works without a GPU).
+int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
+  if (d == nullptr) return fail(TS_ERR_VALUE, "null chain descriptor");
+  const int bn = tile_n_of(d);
+  if (bn != 64 && bn != 128 && bn != 256)
+    return fail(TS_ERR_VALUE, "tile_n must be 64, 128 or 256 (got %d)", d->tile_n);
+  if (d->n_stages < 1 || d->n_stages > TS_MAX_STAGES)
+    return fail(TS_ERR_CONFIG, "n_stages must be in [1, %d]", TS_MAX_STAGES);
+  if (d->n_deps < 0 || d->n_deps > TS_MAX_DEPS)
+    return fail(TS_ERR_CONFIG, "n_deps must be in [0, %d]", TS_MAX_DEPS);
+  if (d->mode != TS_MODE_STREAM && d->mode != TS_MODE_FUSED)
+    return fail(TS_ERR_CONFIG, "unknown mode %d", d->mode);
+  std::memset(p, 0, sizeof(*p));
+  p->n_stages = d->n_stages;
+  p->n_deps = d->n_deps;
+  p->flags = d->flags;
+  p->scratch = d->scratch;
+  p->trace = static_cast<ts_trace_rec*>(d->trace);
+  p->trace_cap = d->trace ? d->trace_cap : 0;
+  const int dtype = d->stages[0].dtype;
+  int items = 0;
+  for (int s = 0; s < d->n_stages; ++s) {
+    const ts_stage_desc& st = d->stages[s];
+    ts::StageParams& sp = p->st[s];
+    if (st.dtype != TS_DTYPE_F16 && st.dtype != TS_DTYPE_BF16)
+      return fail(TS_ERR_TYPE, "stage %d: unknown dtype %d", s, st.dtype);
+    if (st.dtype != dtype) return fail(TS_ERR_CONFIG, "stage %d: all stages must share a dtype", s);
+    if (st.epilogue < TS_EPI_NONE || st.epilogue > TS_EPI_SWIGLU)
+      return fail(TS_ERR_TYPE, "stage %d: unknown epilogue %d", s, st.epilogue);
+    if (st.m < 1 || st.n < 1 || st.k < 1)
+      return fail(TS_ERR_VALUE, "stage %d: m, n, k must be >= 1", s);
+    if (st.n % bn != 0)
+      return fail(TS_ERR_CONFIG, "stage %d: n=%d is not a multiple of tile_n=%d", s, st.n, bn);
+    if (st.k % ts::kBK != 0)
+      return fail(TS_ERR_CONFIG, "stage %d: k=%d is not a multiple of %d", s, st.k, ts::kBK);
+    const int n_out = st.epilogue == TS_EPI_SWIGLU ? st.n / 2 : st.n;
+    if (st.lda < st.k || st.ldb < st.k || st.ldc < n_out || st.lda % 8 || st.ldb % 8 || st.ldc % 8)
+      return fail(TS_ERR_VALUE, "stage %d: leading dimensions must cover the rows and be multiples of 8", s);
+    if (!st.a || !st.b || !st.c) return fail(TS_ERR_VALUE, "stage %d: null operand pointer", s);
+    if ((reinterpret_cast<uintptr_t>(st.a) | reinterpret_cast<uintptr_t>(st.b) |
+         reinterpret_cast<uintptr_t>(st.c)) & 15)
+      return fail(TS_ERR_VALUE, "stage %d: operands must be 16-byte aligned", s);
+    sp.c = st.c;
+    sp.m = st.m;
+    sp.n = st.n;
+    sp.k = st.k;
+    sp.ldc = st.ldc;
+    sp.grid_x = (st.m + ts::kBM - 1) / ts::kBM;
+    sp.grid_y = st.n / bn;
+    if (st.order != TS_ORDER_ROW_MAJOR && st.order != TS_ORDER_STRIDED_ROW_MAJOR)
+      return fail(TS_ERR_TYPE, "stage %d: unknown order %d", s, st.order);
+    if (st.order == TS_ORDER_STRIDED_ROW_MAJOR &&
+        (st.order_stride < 1 || sp.grid_y % st.order_stride != 0))
+      return fail(TS_ERR_CONFIG, "stage %d: order stride %d does not divide grid columns %d", s,
+                  st.order_stride, sp.grid_y);
+    sp.order = st.order;
+    sp.order_stride = st.order == TS_ORDER_STRIDED_ROW_MAJOR ? st.order_stride : 1;
+    sp.epilogue = st.epilogue;
+    sp.k_blocks = st.k / ts::kBK;
+    sp.item_begin = items;
+    items += sp.grid_x * sp.grid_y;
+    sp.item_end = items;
+    sp.in_dep = -1;
+    sp.n_out_deps = 0;
+    if (with_tmaps) {
+      int r = make_tmap(&sp.tmap_a, st.a, st.m, st.k, st.lda, st.dtype, ts::kBM);
+      if (r) return r;
+      r = make_tmap(&sp.tmap_b, st.b, st.n, st.k, st.ldb, st.dtype, bn);
+      if (r) return r;
+    }
+  }
+  p->total_items = items;
+  for (int i = 0; i < d->n_deps; ++i) {
+    const ts_dep_desc& dd = d->deps[i];
+    if (dd.producer < 0 || dd.producer >= d->n_stages || dd.consumer < 0 ||
+        dd.consumer >= d->n_stages)
+      return fail(TS_ERR_CONFIG, "dependency %d names an unknown stage", i);
+    if (dd.producer >= dd.consumer)
+      return fail(TS_ERR_CONFIG,
+                  "dependency %d: producer must be invoked before consumer (cycles are not allowed)", i);
+    if (dd.operand != 0)
+      return fail(TS_ERR_CONFIG, "dependency %d: GeMM stages only consume operand A", i);
+    const ts::StageParams& ps = p->st[dd.producer];
+    ts::StageParams& cs = p->st[dd.consumer];
+    const ts::Grid3 pg{ps.grid_x, ps.grid_y, 1};
+    int r = ts::policy_check(dd.policy, dd.param, pg);
+    if (r == ts::kType) return fail(TS_ERR_TYPE, "dependency %d: unknown policy %d", i, dd.policy);
+    if (r) return fail(TS_ERR_CONFIG, "dependency %d: policy parameter %d invalid for producer grid %dx%d", i, dd.param, pg.x, pg.y);
+    if (cs.grid_x > ps.grid_x)
+      return fail(TS_ERR_CONFIG, "dependency %d: consumer rows %d exceed producer rows %d", i,
+                  cs.grid_x, ps.grid_x);
+    if (cs.in_dep >= 0)
+      return fail(TS_ERR_CONFIG, "dependency %d: stage %d already has an operand-A dependency", i, dd.consumer);
+    const int cols = out_tile_cols(d->stages[dd.producer], bn);
+    if (d->stages[dd.consumer].k != ps.n / bn * cols)
+      return fail(TS_ERR_CONFIG, "dependency %d: consumer k=%d must equal producer output columns %d", i,
+                  d->stages[dd.consumer].k, ps.n / bn * cols);
+    int kb_per_kstep = cols / ts::kBK;
+    int k_steps = cs.k_blocks / kb_per_kstep;
+    if (dd.policy == ts::kConv2D) {
+      if (kb_per_kstep % dd.param != 0)
+        return fail(TS_ERR_CONFIG, "dependency %d: kk=%d does not divide the %d K-blocks of a producer tile", i, dd.param, kb_per_kstep);
+      kb_per_kstep /= dd.param;
+      k_steps *= dd.param;
+    }
+    if (dd.policy == ts::kTile && k_steps > ps.grid_y)
+      return fail(TS_ERR_CONFIG, "dependency %d: tile sync needs one producer column per consumer k-step (%d > %d)", i, k_steps, ps.grid_y);
+    if (d->mode == TS_MODE_FUSED && dd.sem == nullptr)
+      return fail(TS_ERR_VALUE, "dependency %d: null semaphore array", i);
+    ts::DepParams& dp = p->dep[i];
+    dp.sem = dd.sem;
+    dp.policy = dd.policy;
+    dp.param = dd.param;
+    dp.pgx = pg.x;
+    dp.pgy = pg.y;
+    dp.pgz = 1;
+    dp.kb_per_kstep = kb_per_kstep;
+    dp.sem_n = ts::sem_count(dd.policy, dd.param, pg);
+    cs.in_dep = i;
+    ts::StageParams& pw = p->st[dd.producer];
+    pw.out_deps[pw.n_out_deps++] = i;
+  }
+  return TS_OK;
+}
+
+__global__ void wait_kernel(const int* flags, int n) {
+  for (int i = 0; i < n; ++i) {
+    while (ts::ptx::ld_acquire_gpu(flags + i) == 0) __nanosleep(100);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int ts_abi_version(void) { return TS_ABI_VERSION; }
+
+const char* ts_last_error(void) { return g_err.c_str(); }
+
+int ts_sem_count(int policy, int param, int gx, int gy, int gz, int* out) {
+  if (gx < 1 || gy < 1 || gz < 1) return fail(TS_ERR_VALUE, "grid dimensions must be >= 1");
+  const ts::Grid3 g{gx, gy, gz};
+  int r = ts::policy_check(policy, param, g);
+  if (r == ts::kType) return fail(TS_ERR_TYPE, "unknown policy %d", policy);
+  if (r) {
+    if (policy == ts::kStrided && param < 1) return fail(TS_ERR_CONFIG, "stride must be >= 1");
+    if (policy == ts::kStrided)
+      return fail(TS_ERR_CONFIG, "stride %d does not divide producer columns %d", param, gy);
+    return fail(TS_ERR_CONFIG, "kk must be >= 1");
+  }
+  *out = ts::sem_count(policy, param, g);
+  return TS_OK;
+}
+
+int ts_post_target(int policy, int param, int tx, int ty, int tz, int gx, int gy, int gz,
+                   int* out) {
+  const ts::Grid3 g{gx, gy, gz};
+  if (!g.contains(tx, ty, tz))
+    return fail(TS_ERR_VALUE, "tile (%d, %d, %d) outside producer grid %dx%dx%d", tx, ty, tz, gx,
+                gy, gz);
+  if (policy < ts::kTile || policy > ts::kConv2D) return fail(TS_ERR_TYPE, "unknown policy %d", policy);
+  if (policy == ts::kStrided && param == 0) return fail(TS_ERR_VALUE, "stride must be nonzero");
+  *out = ts::post_target(policy, param, tx, ty, g);
+  return TS_OK;
+}
+
+int ts_consumer_wait(int policy, int param, int tx, int ty, int tz, int k_step, int pgx, int pgy,
+                     int pgz, int producer_z, int* sem, int* expected) {
+  (void)tz;
+  (void)pgz;
+  if (policy < ts::kTile || policy > ts::kConv2D) return fail(TS_ERR_TYPE, "unknown policy %d", policy);
+  if ((policy == ts::kStrided || policy == ts::kConv2D) && param == 0)
+    return fail(TS_ERR_VALUE, "policy parameter must be nonzero");
+  ts::Wait w = ts::consumer_wait(policy, param, tx, ty, k_step, ts::Grid3{pgx, pgy, pgz}, producer_z);
+  *sem = w.sem;
+  *expected = w.expected;
+  return TS_OK;
+}
+
+int ts_wait_steps(int policy, int param, int k_steps, int* out, int cap, int* n) {
+  if (policy < ts::kTile || policy > ts::kConv2D) return fail(TS_ERR_TYPE, "unknown policy %d", policy);
+  if (policy == ts::kConv2D && param < 1) return fail(TS_ERR_VALUE, "kk must be >= 1");
+  int c = 0;
+  if (policy == ts::kRow || policy == ts::kStrided) {
+    // Row/Strided wait exactly once, at k-step 0 (policies.py:173-175), whatever k_steps is.
+    if (cap > 0) out[0] = 0;
+    c = 1;
+  } else {
+    for (int k = 0; k < k_steps; ++k) {
+      if (ts::waits_at(policy, param, k)) {
+        if (c < cap) out[c] = k;
+        ++c;
+      }
+    }
+  }
+  *n = c;
+  return c > cap ? fail(TS_ERR_VALUE, "output capacity %d too small (%d steps)", cap, c) : TS_OK;
+}
+
+int ts_order_tile(int order, int stride, int gx, int gy, int gz, int counter, int* x, int* y,
+                  int* z) {
+  const ts::Grid3 g{gx, gy, gz};
+  if (counter < 0 || counter >= g.total())
+    return fail(TS_ERR_VALUE, "counter %d outside grid %dx%dx%d", counter, gx, gy, gz);
+  if (order != ts::kRowMajor && order != ts::kStridedRowMajor)
+    return fail(TS_ERR_TYPE, "unknown order %d", order);
+  if (order == ts::kStridedRowMajor && (stride < 1 || gy % stride != 0))
+    return fail(TS_ERR_CONFIG, "stride %d does not divide grid columns %d", stride, gy);
+  ts::order_tile(order, stride, g, counter, x, y, z);
+  return TS_OK;
+}
+
+int ts_avoid_wait_kernel(int prod_tiles, int prod_occ, int cons_tiles, int cons_occ, int num_sms,
+                         int* out) {
+  *out = ts::avoid_wait_kernel(prod_tiles, prod_occ, cons_tiles, cons_occ, num_sms) ? 1 : 0;
+  return TS_OK;
+}
+
+int ts_chain_grid(const ts_chain_desc* desc, int s, int* gx, int* gy) {
+  static thread_local ts::ChainParams p;
+  int r = build_params(desc, &p, false);
+  if (r) return r;
+  if (s < 0 || s >= p.n_stages) return fail(TS_ERR_VALUE, "stage %d out of range", s);
+  *gx = p.st[s].grid_x;
+  *gy = p.st[s].grid_y;
+  return TS_OK;
+}
+
+int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
+  static thread_local ts::ChainParams p;
+  int r = build_params(desc, &p, true);
+  if (r) return r;
+  if (desc->scratch == nullptr) return fail(TS_ERR_VALUE, "null scratch buffer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int bn = tile_n_of(desc);
+  const int dtype = desc->stages[0].dtype;
+  int ctas = desc->num_ctas > 0 ? desc->num_ctas : sm_count();
+  if (ctas <= 0) return fail(TS_ERR_CUDA, "could not query the SM count");
+  if (desc->mode == TS_MODE_FUSED) {
+    p.item_lo = 0;
+    p.item_hi = p.total_items;
+    int grid = ctas < p.total_items ? ctas : p.total_items;
+    return launch_dispatch(bn, dtype, p, grid, s);
+  }
+  // Stream mode: the same kernel, one launch per stage, no semaphores — the
+  // stream-synchronized baseline (reference Mode.STREAM engine.py:40-42).
+  ts::ChainParams q = p;
+  q.n_deps = 0;
+  for (int i = 0; i < q.n_stages; ++i) {
+    q.st[i].in_dep = -1;
+    q.st[i].n_out_deps = 0;
+  }
+  for (int i = 0; i < q.n_stages; ++i) {
+    q.item_lo = q.st[i].item_begin;
+    q.item_hi = q.st[i].item_end;
+    const int n = q.item_hi - q.item_lo;
+    r = launch_dispatch(bn, dtype, q, ctas < n ? ctas : n, s);
+    if (r) return r;
+  }
+  return TS_OK;
+}
+
+int ts_wait_kernel_launch(const int* flags, int n, void* stream) {
+  if (flags == nullptr || n < 1) return fail(TS_ERR_VALUE, "wait kernel needs >= 1 flag");
+  wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flags, n);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_fail(e, "wait_kernel launch");
+}
+
+int ts_device_sm_count(int* out) {
+  int n = sm_count();
+  if (n <= 0) return fail(TS_ERR_CUDA, "no CUDA device");
+  *out = n;
+  return TS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,289 @@
+"""The paper's host API on B200: ``CuSync`` / ``CuStage``.
+
+    cs = CuSync(tile_n=256)
+    prod = cs.stage(x, w1, h, epilogue="gelu")            # h  = GeLU(x @ w1^T)
+    cons = cs.stage(h, w2, y)                             # y  = h @ w2^T
+    cs.dependency(RowSync(), prod, cons, operand="a")     # cs.dependency<RowSync>(...)
+    cs.launch()                                           # one persistent launch
+
+A stage is a GeMM ``C = epi(A @ B^T)`` with ``A [m, k]`` and ``B [n, k]`` K-major
+(weights in nn.Linear layout), fp16 or bf16, fp32 accumulate. Every tensor is owned by
+PyTorch; the C ABI borrows the pointers for one stream-ordered launch on the current
+torch stream. Semaphores are ``int32`` tensors, zero on entry; the kernel restores the
+zero invariant on exit (unless ``keep_sems``), so a CuSync can be launched repeatedly
+and captured in a CUDA graph.
+
+Modes
+  * ``"fused"``  — one persistent launch over all stages' tiles; consumers wait on
+    semaphores (the paper's fine-grained synchronization, with the persistent claim
+    order replacing the wait kernel: deadlock-free by construction).
+  * ``"stream"`` — the same kernel, one launch per stage on one stream, no semaphores:
+    the stream-synchronized baseline the paper compares against.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from .engine import Dependency, Event, Mode, Scenario, SimTrace, Stage
+from .errors import ConfigError
+from .gpu import Dim3, GpuConfig
+from .policies import (Conv2DTileSync, RowMajor, SyncPolicy, TileOrder, order_code,
+                       policy_code, sem_count)
+
+BM = 128
+BK = 64
+_EPI = {"none": _lib.TS_EPI_NONE, "gelu": _lib.TS_EPI_GELU, "swiglu": _lib.TS_EPI_SWIGLU}
+_DT = {torch.float16: _lib.TS_DTYPE_F16, torch.bfloat16: _lib.TS_DTYPE_BF16}
+_KINDS = ("scheduled", "wait_begin", "wait_end", "post", "finished")
+# Replay order for events sharing a timestamp: posts before the waits they justify
+# (oracle.py:133-144), and a block's own events in program order.
+_RANK = {"post": 0, "finished": 1, "scheduled": 2, "wait_begin": 3, "wait_end": 4}
+
+
+@dataclass
+class CuStage:
+    """One GeMM stage (the paper's CuStage)."""
+
+    cs: "CuSync"
+    index: int
+    id: str
+    a: torch.Tensor
+    b: torch.Tensor
+    c: torch.Tensor
+    epilogue: str
+    order: TileOrder
+
+    @property
+    def m(self) -> int:
+        return self.a.shape[0]
+
+    @property
+    def n(self) -> int:
+        return self.b.shape[0]
+
+    @property
+    def k(self) -> int:
+        return self.a.shape[1]
+
+    @property
+    def out_tile_cols(self) -> int:
+        return self.cs.tile_n // 2 if self.epilogue == "swiglu" else self.cs.tile_n
+
+    @property
+    def grid(self) -> Dim3:
+        """Tile grid as the reference's Stage.grid sees it (row tiles, column tiles)."""
+        return Dim3(-(-self.m // BM), max(1, self.n // self.cs.tile_n), 1)
+
+    def flops(self) -> int:
+        return 2 * self.m * self.n * self.k
+
+
+@dataclass
+class CuDep:
+    producer: CuStage
+    consumer: CuStage
+    operand: str
+    policy: SyncPolicy
+    sem: torch.Tensor
+
+    @property
+    def id(self) -> str:
+        return f"{self.producer.id}->{self.consumer.id}/{self.operand}"
+
+
+@dataclass
+class CuSync:
+    """A chain of dependent GeMM stages launched through libtilesync_b200.so."""
+
+    tile_n: int = 256
+    mode: str = "fused"
+    reorder: bool = True
+    watchdog: bool = True
+    keep_sems: bool = False
+    num_ctas: int = 0
+    device: torch.device | None = None
+    stages: list[CuStage] = field(default_factory=list)
+    deps: list[CuDep] = field(default_factory=list)
+
+    def __post_init__(self) -> None:
+        if self.mode not in ("fused", "stream"):
+            raise ConfigError(f"mode must be 'fused' or 'stream', got {self.mode!r}")
+        if self.tile_n not in (64, 128, 256):
+            raise ConfigError(f"tile_n must be 64, 128 or 256, got {self.tile_n}")
+        self._desc: _lib.ChainDesc | None = None
+        self._scratch: torch.Tensor | None = None
+        self._trace: torch.Tensor | None = None
+        self._trace_cap = 0
+
+    # -- construction ---------------------------------------------
+    def stage(self, a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, epilogue: str = "none",
+              order: TileOrder = RowMajor(), id: str | None = None) -> CuStage:
+        if len(self.stages) >= _lib.TS_MAX_STAGES:
+            raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
+        if epilogue not in _EPI:
+            raise ConfigError(f"unknown epilogue {epilogue!r}")
+        for t, name in ((a, "a"), (b, "b"), (c, "c")):
+            if t.dim() != 2 or t.stride(1) != 1:
+                raise ValueError(f"{name} must be a row-major 2-D tensor")
+            if t.dtype not in _DT:
+                raise TypeError(f"{name}: dtype {t.dtype} unsupported (fp16/bf16)")
+            if not t.is_cuda:
+                raise ValueError(f"{name} must be a CUDA tensor")
+        if a.shape[1] != b.shape[1]:
+            raise ValueError(f"inner dimensions differ: a {tuple(a.shape)} b {tuple(b.shape)}")
+        n_out = b.shape[0] // 2 if epilogue == "swiglu" else b.shape[0]
+        if c.shape[0] != a.shape[0] or c.shape[1] != n_out:
+            raise ValueError(f"c must be [{a.shape[0]}, {n_out}], got {tuple(c.shape)}")
+        st = CuStage(self, len(self.stages), id or f"gemm{len(self.stages) + 1}", a, b, c,
+                     epilogue, order)
+        self.stages.append(st)
+        self.device = a.device
+        self._desc = None
+        return st
+
+    def dependency(self, policy: SyncPolicy, producer: CuStage, consumer: CuStage,
+                   operand: str = "a") -> CuDep:
+        """cs.dependency<Policy>(prod, cons, operand) — allocates the semaphore array."""
+        if len(self.deps) >= _lib.TS_MAX_DEPS:
+            raise ConfigError(f"at most {_lib.TS_MAX_DEPS} dependencies per chain")
+        n = sem_count(policy, producer.grid)
+        sem = torch.zeros(n, dtype=torch.int32, device=producer.a.device)
+        d = CuDep(producer, consumer, operand, policy, sem)
+        self.deps.append(d)
+        self._desc = None
+        return d
+
+    # -- reference view (for the oracle and the planner) ------------------------------
+    def scenario(self, num_sms: int = 148) -> Scenario:
+        """The reference Scenario this chain executes, with B200 grids."""
+        in_dep = {d.consumer.index: d for d in self.deps}
+        stages = []
+        for st in self.stages:
+            d = in_dep.get(st.index)
+            if d is None:
+                k_steps = max(1, st.k // st.out_tile_cols)
+            else:
+                k_steps = st.k // d.producer.out_tile_cols
+                if isinstance(d.policy, Conv2DTileSync):
+                    k_steps *= d.policy.kk
+            stages.append(Stage(id=st.id, grid=st.grid, occupancy=1, k_steps=k_steps,
+                                order=st.order))
+        deps = tuple(Dependency(d.producer.id, d.consumer.id, d.operand, d.policy)
+                     for d in self.deps)
+        mode = Mode.FINE if self.mode == "fused" else Mode.STREAM
+        return Scenario(gpu=GpuConfig(num_sms), stages=tuple(stages), deps=deps, mode=mode)
+
+    # -- launch ------------------------------------------------------------------------
+    def _build(self) -> _lib.ChainDesc:
+        if not self.stages:
+            raise ConfigError("chain has no stages")
+        d = _lib.ChainDesc()
+        d.n_stages = len(self.stages)
+        for i, st in enumerate(self.stages):
+            sd = d.stages[i]
+            sd.a, sd.b, sd.c = st.a.data_ptr(), st.b.data_ptr(), st.c.data_ptr()
+            sd.m, sd.n, sd.k = st.m, st.n, st.k
+            sd.lda, sd.ldb, sd.ldc = st.a.stride(0), st.b.stride(0), st.c.stride(0)
+            sd.dtype = _DT[st.a.dtype]
+            sd.epilogue = _EPI[st.epilogue]
+            sd.order, sd.order_stride = order_code(st.order)
+        d.n_deps = len(self.deps)
+        for i, dep in enumerate(self.deps):
+            dd = d.deps[i]
+            dd.producer, dd.consumer = dep.producer.index, dep.consumer.index
+            if dep.operand != "a":
+                raise ConfigError("GeMM stages consume their producer through operand 'a'")
+            dd.operand = 0
+            dd.policy, dd.param = policy_code(dep.policy)
+            dd.sem = dep.sem.data_ptr()
+        d.mode = _lib.TS_MODE_FUSED if self.mode == "fused" else _lib.TS_MODE_STREAM
+        d.tile_n = self.tile_n
+        d.flags = ((0 if self.reorder else _lib.TS_FLAG_NO_REORDER)
+                   | (0 if self.watchdog else _lib.TS_FLAG_NO_WATCHDOG)
+                   | (_lib.TS_FLAG_KEEP_SEMS if self.keep_sems else 0))
+        d.num_ctas = self.num_ctas
+        if self._scratch is None:
+            self._scratch = torch.zeros(_lib.TS_SCRATCH_INTS, dtype=torch.int32,
+                                        device=self.device)
+        d.scratch = self._scratch.data_ptr()
+        d.trace = None
+        d.trace_cap = 0
+        return d
+
+    def enable_trace(self, capacity: int | None = None) -> None:
+        """Record the reference's per-block events on the device (engine.py:220-248)."""
+        if capacity is None:
+            capacity = 0
+            for st in self.stages:
+                capacity += st.grid.total() * (3 + 2 * 2 * max(1, st.k // BK))
+        self._trace_cap = capacity
+        self._trace = torch.zeros(capacity * _lib.TRACE_REC_BYTES, dtype=torch.uint8,
+                                  device=self.device)
+        self._desc = None
+
+    def launch(self, stream: torch.cuda.Stream | None = None) -> None:
+        """Enqueue the chain on `stream` (default: the current torch stream)."""
+        if self._desc is None:
+            self._desc = self._build()
+            if self._trace is not None:
+                self._desc.trace = self._trace.data_ptr()
+                self._desc.trace_cap = self._trace_cap
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if self._trace is not None:
+            self._scratch[2].zero_()
+        _lib.check(_lib.load().ts_chain_launch(ctypes.byref(self._desc),
+                                               ctypes.c_void_p(s.cuda_stream)))
+
+    __call__ = launch
+
+    # -- results -------------------------------------------------------------------------
+    def watchdog_fired(self) -> bool:
+        """True if a semaphore wait timed out (the device analogue of detect_deadlock,
+        engine.py:614-637). Synchronizes."""
+        return bool(self._scratch is not None and int(self._scratch[3].item()) != 0)
+
+    def final_semaphores(self) -> dict[str, tuple[int, ...]]:
+        """Semaphore values after a ``keep_sems=True`` launch (SimTrace.final_semaphores)."""
+        return {d.id: tuple(int(v) for v in d.sem.cpu().tolist()) for d in self.deps}
+
+    def reset_semaphores(self) -> None:
+        for d in self.deps:
+            d.sem.zero_()
+
+    def trace_events(self) -> list[Event]:
+        """The device trace as reference Events, times in ns from the first event."""
+        if self._trace is None:
+            raise RuntimeError("tracing is not enabled (call enable_trace() first)")
+        n = min(int(self._scratch[2].item()), self._trace_cap)
+        raw = self._trace[: n * _lib.TRACE_REC_BYTES].cpu().numpy().tobytes()
+        recs = (_lib.TraceRec * n).from_buffer_copy(raw) if n else []
+        if n and int(self._scratch[2].item()) > self._trace_cap:
+            raise RuntimeError("trace buffer overflowed")
+        t0 = min((r.t_ns for r in recs), default=0)
+        dep_ids = [d.id for d in self.deps]
+        evs = []
+        for i, r in enumerate(recs):
+            kind = _KINDS[r.kind]
+            ev = Event(time=int(r.t_ns - t0), stage=self.stages[r.stage].id, tb=r.tb, kind=kind,
+                       tile=(r.x, r.y, r.z),
+                       k=r.k if r.k >= 0 else None,
+                       dep=dep_ids[r.dep] if r.dep >= 0 else None,
+                       sem=r.sem if r.sem >= 0 else None,
+                       expected=r.value if kind in ("wait_begin", "wait_end") else None,
+                       value=r.value if kind == "post" else None)
+            evs.append((ev.time, _RANK[kind], i, ev))
+        evs.sort(key=lambda e: e[:3])
+        return [e[3] for e in evs]
+
+    def sim_trace(self) -> SimTrace:
+        mode = Mode.FINE if self.mode == "fused" else Mode.STREAM
+        return SimTrace(mode=mode, events=self.trace_events(),
+                        final_semaphores=self.final_semaphores())
+
+    def flops(self) -> int:
+        return sum(st.flops() for st in self.stages)
