@@ -140,6 +140,8 @@ typedef struct {
   ts_dep_desc deps[TS_MAX_DEPS];
   int mode;      /* ts_mode */
   int tile_n;    /* 64, 128 or 256; 0 = 256 */
+  int cta_group; /* 1: one CTA per 128-row tile; 2: CTA pair per 256-row tile
+                    (tcgen05 cta_group::2); 0 = 2 */
   int flags;     /* ts_flags bitmask */
   int num_ctas;  /* persistent CTAs; 0 = one per SM */
   int* scratch;  /* device int32[TS_SCRATCH_INTS], zero on first use; kernels restore it */

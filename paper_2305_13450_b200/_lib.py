@@ -59,7 +59,8 @@ class ChainDesc(ctypes.Structure):
     _fields_ = [
         ("n_stages", ctypes.c_int), ("stages", StageDesc * TS_MAX_STAGES),
         ("n_deps", ctypes.c_int), ("deps", DepDesc * TS_MAX_DEPS),
-        ("mode", ctypes.c_int), ("tile_n", ctypes.c_int), ("flags", ctypes.c_int),
+        ("mode", ctypes.c_int), ("tile_n", ctypes.c_int), ("cta_group", ctypes.c_int),
+        ("flags", ctypes.c_int),
         ("num_ctas", ctypes.c_int), ("scratch", ctypes.c_void_p),
         ("trace", ctypes.c_void_p), ("trace_cap", ctypes.c_int),
     ]

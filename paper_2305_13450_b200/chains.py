@@ -23,13 +23,14 @@ class MlpChain:
 
     def __init__(self, x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor,
                  policy: SyncPolicy = RowSync(), mode: str = "fused", tile_n: int = 256,
-                 reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0):
+                 reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0,
+                 extra_flags: int = 0, cta_group: int = 2):
         m = x.shape[0]
         self.x, self.w1, self.w2 = x, w1, w2
         self.h = torch.empty(m, w1.shape[0], dtype=x.dtype, device=x.device)
         self.y = torch.empty(m, w2.shape[0], dtype=x.dtype, device=x.device)
         self.cs = CuSync(tile_n=tile_n, mode=mode, reorder=reorder, keep_sems=keep_sems,
-                         num_ctas=num_ctas)
+                         num_ctas=num_ctas, extra_flags=extra_flags, cta_group=cta_group)
         self.prod = self.cs.stage(x, w1, self.h, epilogue="gelu", id="gemm1")
         self.cons = self.cs.stage(self.h, w2, self.y, id="gemm2")
         self.dep = self.cs.dependency(policy, self.prod, self.cons, operand="a")
@@ -62,13 +63,14 @@ class SwigluChain:
 
     def __init__(self, x: torch.Tensor, w_gate_up: torch.Tensor, w_down: torch.Tensor,
                  policy: SyncPolicy = RowSync(), mode: str = "fused", tile_n: int = 256,
-                 reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0):
+                 reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0,
+                 cta_group: int = 2):
         m = x.shape[0]
         f = w_gate_up.shape[0] // 2
         self.h = torch.empty(m, f, dtype=x.dtype, device=x.device)
         self.y = torch.empty(m, w_down.shape[0], dtype=x.dtype, device=x.device)
         self.cs = CuSync(tile_n=tile_n, mode=mode, reorder=reorder, keep_sems=keep_sems,
-                         num_ctas=num_ctas)
+                         num_ctas=num_ctas, cta_group=cta_group)
         self.prod = self.cs.stage(x, w_gate_up, self.h, epilogue="swiglu", id="gate_up")
         self.cons = self.cs.stage(self.h, w_down, self.y, id="down")
         self.dep = self.cs.dependency(policy, self.prod, self.cons, operand="a")

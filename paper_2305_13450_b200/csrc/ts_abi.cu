@@ -80,40 +80,58 @@ int sm_count() {
   return n;
 }
 
-template <int BN, typename T>
-int launch_one(const ts::ChainParams& p, int grid, cudaStream_t stream) {
-  using C = ts::Cfg<BN>;
+// `units` = tiles in flight at once (CTAs for CG=1, CTA pairs for CG=2).
+template <int BN, int CG, typename T>
+int launch_one(const ts::ChainParams& p, int units, cudaStream_t stream) {
+  using C = ts::Cfg<BN, CG>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(ts::chain_kernel<BN, T>,
+    attr_err = cudaFuncSetAttribute(ts::chain_kernel<BN, CG, T>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   });
   if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
-  ts::chain_kernel<BN, T><<<grid, ts::kThreads, C::kSmemBytes, stream>>>(p);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * CG, 1, 1);
+  cfg.blockDim = dim3(ts::kThreads, 1, 1);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, ts::chain_kernel<BN, CG, T>, p);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "chain_kernel launch");
   return TS_OK;
 }
 
-int launch_dispatch(int bn, int dtype, const ts::ChainParams& p, int grid, cudaStream_t s) {
-  if (dtype == TS_DTYPE_BF16) {
-    switch (bn) {
-      case 64: return launch_one<64, __nv_bfloat16>(p, grid, s);
-      case 128: return launch_one<128, __nv_bfloat16>(p, grid, s);
-      case 256: return launch_one<256, __nv_bfloat16>(p, grid, s);
-    }
-  } else {
-    switch (bn) {
-      case 64: return launch_one<64, __half>(p, grid, s);
-      case 128: return launch_one<128, __half>(p, grid, s);
-      case 256: return launch_one<256, __half>(p, grid, s);
-    }
+template <int CG, typename T>
+int launch_bn(int bn, const ts::ChainParams& p, int units, cudaStream_t s) {
+  switch (bn) {
+    case 64: return launch_one<64, CG, T>(p, units, s);
+    case 128: return launch_one<128, CG, T>(p, units, s);
+    case 256: return launch_one<256, CG, T>(p, units, s);
   }
   return fail(TS_ERR_VALUE, "tile_n must be 64, 128 or 256 (got %d)", bn);
 }
 
+int launch_dispatch(int bn, int cg, int dtype, const ts::ChainParams& p, int units,
+                    cudaStream_t s) {
+  if (cg == 2) {
+    if (bn == 64) return fail(TS_ERR_VALUE, "cta_group 2 needs tile_n >= 128");
+    return dtype == TS_DTYPE_BF16 ? launch_bn<2, __nv_bfloat16>(bn, p, units, s)
+                                  : launch_bn<2, __half>(bn, p, units, s);
+  }
+  return dtype == TS_DTYPE_BF16 ? launch_bn<1, __nv_bfloat16>(bn, p, units, s)
+                                : launch_bn<1, __half>(bn, p, units, s);
+}
+
 int tile_n_of(const ts_chain_desc* d) { return d->tile_n == 0 ? 256 : d->tile_n; }
+int cta_group_of(const ts_chain_desc* d) { return d->cta_group == 0 ? 2 : d->cta_group; }
 
 // Output columns one tile of stage `st` writes (the producer "column tile" width that a
 // consumer k-step covers).
@@ -128,6 +146,10 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
   const int bn = tile_n_of(d);
   if (bn != 64 && bn != 128 && bn != 256)
     return fail(TS_ERR_VALUE, "tile_n must be 64, 128 or 256 (got %d)", d->tile_n);
+  const int cg = cta_group_of(d);
+  if (cg != 1 && cg != 2) return fail(TS_ERR_VALUE, "cta_group must be 1 or 2 (got %d)", d->cta_group);
+  if (cg == 2 && bn == 64) return fail(TS_ERR_VALUE, "cta_group 2 needs tile_n >= 128");
+  const int tile_m = 128 * cg;
   if (d->n_stages < 1 || d->n_stages > TS_MAX_STAGES)
     return fail(TS_ERR_CONFIG, "n_stages must be in [1, %d]", TS_MAX_STAGES);
   if (d->n_deps < 0 || d->n_deps > TS_MAX_DEPS)
@@ -169,7 +191,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.n = st.n;
     sp.k = st.k;
     sp.ldc = st.ldc;
-    sp.grid_x = (st.m + ts::kBM - 1) / ts::kBM;
+    sp.grid_x = (st.m + tile_m - 1) / tile_m;
     sp.grid_y = st.n / bn;
     if (st.order != TS_ORDER_ROW_MAJOR && st.order != TS_ORDER_STRIDED_ROW_MAJOR)
       return fail(TS_ERR_TYPE, "stage %d: unknown order %d", s, st.order);
@@ -187,9 +209,9 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.in_dep = -1;
     sp.n_out_deps = 0;
     if (with_tmaps) {
-      int r = make_tmap(&sp.tmap_a, st.a, st.m, st.k, st.lda, st.dtype, ts::kBM);
+      int r = make_tmap(&sp.tmap_a, st.a, st.m, st.k, st.lda, st.dtype, 128);
       if (r) return r;
-      r = make_tmap(&sp.tmap_b, st.b, st.n, st.k, st.ldb, st.dtype, bn);
+      r = make_tmap(&sp.tmap_b, st.b, st.n, st.k, st.ldb, st.dtype, bn / cg);
       if (r) return r;
     }
   }
@@ -357,14 +379,17 @@ int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
   if (desc->scratch == nullptr) return fail(TS_ERR_VALUE, "null scratch buffer");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int bn = tile_n_of(desc);
+  const int cg = cta_group_of(desc);
   const int dtype = desc->stages[0].dtype;
   int ctas = desc->num_ctas > 0 ? desc->num_ctas : sm_count();
   if (ctas <= 0) return fail(TS_ERR_CUDA, "could not query the SM count");
+  ctas /= cg;  // tiles in flight: CTAs (cg = 1) or CTA pairs (cg = 2)
+  if (ctas < 1) return fail(TS_ERR_VALUE, "num_ctas too small for cta_group %d", cg);
   if (desc->mode == TS_MODE_FUSED) {
     p.item_lo = 0;
     p.item_hi = p.total_items;
     int grid = ctas < p.total_items ? ctas : p.total_items;
-    return launch_dispatch(bn, dtype, p, grid, s);
+    return launch_dispatch(bn, cg, dtype, p, grid, s);
   }
   // Stream mode: the same kernel, one launch per stage, no semaphores — the
   // stream-synchronized baseline (reference Mode.STREAM engine.py:40-42).
@@ -378,7 +403,7 @@ int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
     q.item_lo = q.st[i].item_begin;
     q.item_hi = q.st[i].item_end;
     const int n = q.item_hi - q.item_lo;
-    r = launch_dispatch(bn, dtype, q, ctas < n ? ctas : n, s);
+    r = launch_dispatch(bn, cg, dtype, q, ctas < n ? ctas : n, s);
     if (r) return r;
   }
   return TS_OK;

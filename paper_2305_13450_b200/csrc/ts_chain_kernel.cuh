@@ -8,17 +8,22 @@
 // (engine.py:183-204). Within a stage, the n-th claim computes tile
 // order_tile(order, grid, n) (the paper's stage.tile(); policies.py:181).
 //
-// Per CTA (256 threads, one CTA per SM):
-//   warp 0 lane 0 : scheduler + TMA producer. For a consumer tile it issues the weight
-//                   (B) tile first, then spins on the policy's semaphore (ld.acquire.gpu)
-//                   and issues the dependent A tile ("+R", PAPER.md:534-540;
-//                   kstep_duration engine.py:207-217).
-//   warp 1        : tcgen05.mma issuer (one lane), fp32 accumulators in TMEM,
+// CG = 1: one CTA per tile (UMMA M = 128). CG = 2: a CTA pair (cluster of 2 on one TPC)
+// per tile, UMMA M = 256 with cta_group::2: each CTA loads its 128 rows of A and half
+// of the B tile, halving per-SM operand traffic; the leader CTA issues the MMAs.
+//
+// Roles (256 threads per CTA):
+//   warp 0 lane 0 : scheduler (leader) + TMA producer. For a consumer tile it issues the
+//                   weight (B) tile first, then spins on the policy's semaphore
+//                   (ld.acquire.gpu) and issues the dependent A tile ("+R",
+//                   PAPER.md:534-540; kstep_duration engine.py:207-217).
+//   warp 1        : tcgen05.mma issuer (leader only), fp32 accumulators in TMEM,
 //                   double-buffered so the epilogue of tile i overlaps the mainloop of i+1.
 //   warp 2        : TMEM allocator.
-//   warps 4-7     : epilogue: tcgen05.ld -> GeLU/SwiGLU -> global stores, then one
-//                   thread posts (fence + red.release.gpu) to every outgoing dependency
-//                   (stage.post; post_target policies.py:128-142).
+//   warps 4-7     : epilogue: tcgen05.ld -> GeLU/SwiGLU -> global stores; then the leader
+//                   posts (fence + atom.release.gpu) to every outgoing dependency once the
+//                   whole tile is stored (stage.post, PAPER.md:332,366-370;
+//                   post_target policies.py:128-142).
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -31,7 +36,6 @@
 
 namespace ts {
 
-constexpr int kBM = 128;        // UMMA M (rows of a tile)
 constexpr int kBK = 64;         // K elements per smem stage = one 128-B swizzle row
 constexpr int kThreads = 256;
 constexpr int kTileRing = 4;    // tile-id hand-off ring between scheduler and consumers
@@ -40,7 +44,7 @@ constexpr uint64_t kWatchdogNs = 4000000000ull;
 
 struct StageParams {
   CUtensorMap tmap_a;  // [m, k] K-major, box {64, 128}, 128-B swizzle
-  CUtensorMap tmap_b;  // [n, k] K-major, box {64, BN}, 128-B swizzle
+  CUtensorMap tmap_b;  // [n, k] K-major, box {64, BN/CG}, 128-B swizzle
   void* c;
   int m, n, k, ldc;
   int grid_x, grid_y;
@@ -72,17 +76,22 @@ struct ChainParams {
   int flags;
 };
 
-template <int BN>
+template <int BN, int CG>
 struct Cfg {
-  static constexpr int kStages = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
-  static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kTileM = 128 * CG;            // rows of a (pair) tile
+  static constexpr int kBRows = BN / CG;             // B rows each CTA loads
+  static constexpr int kABytes = 128 * kBK * 2;
+  static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
+  static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kTmemCols = 2 * BN;           // two accumulator buffers
   static constexpr int kBarOffset = kStages * kStageBytes;
-  // full, empty per stage; tmem full/empty x2; tile ring full/empty x kTileRing
-  static constexpr int kNumBars = 2 * kStages + 4 + 2 * kTileRing;
+  // full, empty per stage; tmem full/empty x2; tile ring full/empty; peer_done x2
+  static constexpr int kNumBars = 2 * kStages + 4 + 2 * kTileRing + 2;
   static constexpr int kSmemBytes = 1024 + kBarOffset + kNumBars * 8 + 64;
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+  static_assert(kBRows % 8 == 0 && kBRows <= 256, "B box rows");
 };
 
 __device__ __forceinline__ int stage_of(const ChainParams& p, int g) {
@@ -146,14 +155,17 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
 }
 
 // Spin until sem >= expected (the paper's wait_till, relaxed to >= so
-// the semaphores stay monotone as in SemaphoreArray, policies.py:84-99).
+// the semaphores stay monotone as in SemaphoreArray, policies.py:84-99). Exponential
+// back-off keeps the polling traffic and issue slots of waiting SMs low.
 __device__ __forceinline__ void sem_wait(const ChainParams& p, const int* sem, int expected) {
   if (ptx::ld_acquire_gpu(sem) >= expected) return;
   const bool watchdog = (p.flags & TS_FLAG_NO_WATCHDOG) == 0;
   uint64_t t0 = ptx::global_timer();
+  uint32_t ns = 32;
 #pragma unroll 1
   while (ptx::ld_acquire_gpu(sem) < expected) {
-    __nanosleep(40);
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
     if (watchdog && ptx::global_timer() - t0 > kWatchdogNs) {
       atomicExch(&p.scratch[3], 1);
       return;
@@ -161,15 +173,30 @@ __device__ __forceinline__ void sem_wait(const ChainParams& p, const int* sem, i
   }
 }
 
-template <int BN, typename T>
+struct Tile {
+  int g, s, tb, tx, ty;
+};
+
+__device__ __forceinline__ Tile decode(const ChainParams& p, int g) {
+  Tile t;
+  t.g = g;
+  t.s = stage_of(p, g);
+  const StageParams& st = p.st[t.s];
+  t.tb = g - st.item_begin;
+  int tz;
+  order_tile(st.order, st.order_stride, Grid3{st.grid_x, st.grid_y, 1}, t.tb, &t.tx, &t.ty, &tz);
+  return t;
+}
+
+template <int BN, int CG, typename T>
 __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constant__ ChainParams p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   constexpr int S = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;                       // S x [128 x 64]
-  uint8_t* sB = smem + S * C::kABytes;      // S x [BN x 64]
+  uint8_t* sB = smem + S * C::kABytes;      // S x [BN/CG x 64]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOffset);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
@@ -177,12 +204,15 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
   uint64_t* tmem_empty = tmem_full + 2;
   uint64_t* ti_full = tmem_empty + 2;
   uint64_t* ti_empty = ti_full + kTileRing;
-  int* ti_item = reinterpret_cast<int*>(ti_empty + kTileRing);
+  uint64_t* peer_done = ti_empty + kTileRing;
+  int* ti_item = reinterpret_cast<int*>(peer_done + 2);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ti_item + kTileRing);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? ptx::cluster_rank() : 0;
+  const bool leader = rank == 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -191,11 +221,13 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tmem_full[i], 1);
-      ptx::mbar_init(&tmem_empty[i], kEpiThreads / 32);
+      ptx::mbar_init(&tmem_empty[i], CG * kEpiThreads / 32);
+      ptx::mbar_init(&peer_done[i], 1);
     }
     for (int i = 0; i < kTileRing; ++i) {
       ptx::mbar_init(&ti_full[i], 1);
-      ptx::mbar_init(&ti_empty[i], 1 + kEpiThreads / 32);
+      // leader MMA warp + every epilogue warp of the pair + the peer's producer lane
+      ptx::mbar_init(&ti_empty[i], 1 + CG * kEpiThreads / 32 + (CG - 1));
     }
     ptx::fence_barrier_init();
   }
@@ -205,129 +237,212 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
       ptx::tma_prefetch_desc(&p.st[s].tmap_b);
     }
   }
-  if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 2) ptx::tmem_alloc<C::kTmemCols, CG>(tmem_slot);
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    ptx::cluster_sync();
+  } else {
+    __syncthreads();
+  }
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+
+  // Receive the next tile id from the ring (and release the slot).
+  auto ring_take = [&](int it, bool remote_release) -> int {
+    const int slot = it % kTileRing;
+    if constexpr (CG == 2) {
+      ptx::mbar_wait_cluster(&ti_full[slot], (it / kTileRing) & 1);
+    } else {
+      ptx::mbar_wait(&ti_full[slot], (it / kTileRing) & 1);
+    }
+    const int g = ti_item[slot];
+    __syncwarp();
+    if (lane == 0) {
+      if (remote_release) {
+        ptx::mbar_arrive_remote(ptx::mapa(&ti_empty[slot], 0));
+      } else {
+        ptx::mbar_arrive(&ti_empty[slot]);
+      }
+    }
+    return g;
+  };
 
   if (warp == 0) {
     // ===================== scheduler + TMA producer =====================
     if (lane == 0) {
       const bool reorder = (p.flags & TS_FLAG_NO_REORDER) == 0;
-      const uint64_t pol_stream = ptx::policy_evict_first();  // weights: read once
-      const uint64_t pol_keep = ptx::policy_evict_last();     // activations: reused
+      // L2 hints: activations (A) are re-read by every column tile -> evict_last.
+      // Weights (B) are re-read by every row tile of the same column; they stream once
+      // only when the stage has a single row of tiles -> evict_first there.
+      const uint64_t pol_first = ptx::policy_evict_first();
+      const uint64_t pol_normal = ptx::policy_evict_normal();
+      const uint64_t pol_last = ptx::policy_evict_last();
+      const int b_hint = (p.flags >> 8) & 3;
+      uint32_t full_cluster[S];
+      if constexpr (CG == 2) {
+        for (int i = 0; i < S; ++i) full_cluster[i] = ptx::mapa(&full[i], 0);
+      }
       uint32_t pipe = 0;
 #pragma unroll 1
       for (int it = 0;; ++it) {
+        int g;
         const int slot = it % kTileRing;
-        ptx::mbar_wait(&ti_empty[slot], ((it / kTileRing) & 1) ^ 1);
-        int g = p.item_lo + atomicAdd(&p.scratch[0], 1);
-        if (g >= p.item_hi) g = -1;
-        ti_item[slot] = g;
-        ptx::mbar_arrive(&ti_full[slot]);
+        if (leader) {
+          if constexpr (CG == 2) {
+            ptx::mbar_wait_cluster(&ti_empty[slot], ((it / kTileRing) & 1) ^ 1);
+          } else {
+            ptx::mbar_wait(&ti_empty[slot], ((it / kTileRing) & 1) ^ 1);
+          }
+          g = p.item_lo + atomicAdd(&p.scratch[0], 1);
+          if (g >= p.item_hi) g = -1;
+          ti_item[slot] = g;
+          ptx::mbar_arrive(&ti_full[slot]);
+          if constexpr (CG == 2) {
+            ptx::st_cluster_u32(ptx::mapa(&ti_item[slot], 1), static_cast<uint32_t>(g));
+            ptx::mbar_arrive_remote(ptx::mapa(&ti_full[slot], 1));
+          }
+        } else {
+          ptx::mbar_wait_cluster(&ti_full[slot], (it / kTileRing) & 1);
+          g = ti_item[slot];
+          ptx::mbar_arrive_remote(ptx::mapa(&ti_empty[slot], 0));
+        }
         if (g < 0) break;
-        const int s = stage_of(p, g);
-        const StageParams& st = p.st[s];
-        const int tb = g - st.item_begin;
-        int tx, ty, tz;
-        order_tile(st.order, st.order_stride, Grid3{st.grid_x, st.grid_y, 1}, tb, &tx, &ty, &tz);
-        trace_event(p, ptx::global_timer(), 0, s, tb, -1, -1, -1, -1, tx, ty);
-        const int m0 = tx * kBM;
-        const int n0 = ty * BN;
+        const Tile t = decode(p, g);
+        const StageParams& st = p.st[t.s];
+        if (leader) trace_event(p, ptx::global_timer(), 0, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty);
+        const int m0 = t.tx * C::kTileM + static_cast<int>(rank) * 128;
+        const int n0 = t.ty * BN + static_cast<int>(rank) * C::kBRows;
         const int d = st.in_dep;
+        const int bh = b_hint ? b_hint : (st.grid_x == 1 ? 1 : 2);
+        const uint64_t pol_b = bh == 1 ? pol_first : (bh == 2 ? pol_normal : pol_last);
 #pragma unroll 1
         for (int kb = 0; kb < st.k_blocks; ++kb, ++pipe) {
           const int rs = pipe % S;
           ptx::mbar_wait(&empty[rs], ((pipe / S) & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[rs], C::kStageBytes);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[rs], CG * C::kStageBytes);
           uint8_t* a_dst = sA + rs * C::kABytes;
           uint8_t* b_dst = sB + rs * C::kBBytes;
-          if (reorder) ptx::tma_load_2d(b_dst, &st.tmap_b, &full[rs], kb * kBK, n0, pol_stream);
+          auto load_b = [&]() {
+            if constexpr (CG == 2) {
+              ptx::tma_load_2d_pair(b_dst, &st.tmap_b, full_cluster[rs], kb * kBK, n0, pol_b);
+            } else {
+              ptx::tma_load_2d(b_dst, &st.tmap_b, &full[rs], kb * kBK, n0, pol_b);
+            }
+          };
+          if (reorder) load_b();
           if (d >= 0) {
             const DepParams& dp = p.dep[d];
             if (kb % dp.kb_per_kstep == 0) {
               const int kstep = kb / dp.kb_per_kstep;
-              Wait w = consumer_wait(dp.policy, dp.param, tx, ty, kstep,
+              Wait w = consumer_wait(dp.policy, dp.param, t.tx, t.ty, kstep,
                                      Grid3{dp.pgx, dp.pgy, dp.pgz}, dp.pgz);
               if (w.sem >= 0) {
-                trace_event(p, ptx::global_timer(), 1, s, tb, kstep, d, w.sem, w.expected, tx, ty);
+                if (leader)
+                  trace_event(p, ptx::global_timer(), 1, t.s, t.tb, kstep, d, w.sem, w.expected, t.tx, t.ty);
                 sem_wait(p, dp.sem + w.sem, w.expected);
-                trace_event(p, ptx::global_timer(), 2, s, tb, kstep, d, w.sem, w.expected, tx, ty);
+                if (leader)
+                  trace_event(p, ptx::global_timer(), 2, t.s, t.tb, kstep, d, w.sem, w.expected, t.tx, t.ty);
                 ptx::fence_proxy_async_global();
               }
             }
           }
-          ptx::tma_load_2d(a_dst, &st.tmap_a, &full[rs], kb * kBK, m0, pol_keep);
-          if (!reorder) ptx::tma_load_2d(b_dst, &st.tmap_b, &full[rs], kb * kBK, n0, pol_stream);
+          if constexpr (CG == 2) {
+            ptx::tma_load_2d_pair(a_dst, &st.tmap_a, full_cluster[rs], kb * kBK, m0, pol_last);
+          } else {
+            ptx::tma_load_2d(a_dst, &st.tmap_a, &full[rs], kb * kBK, m0, pol_last);
+          }
+          if (!reorder) load_b();
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== tcgen05.mma issuer =====================
-    constexpr uint32_t kIdesc = ptx::idesc_f16(kBM, BN, AbFormat<T>::value);
-    uint32_t pipe = 0;
-    uint32_t local = 0;
+    // ===================== tcgen05.mma issuer (leader) =====================
+    if (leader) {
+      constexpr uint32_t kIdesc = ptx::idesc_f16(C::kTileM, BN, AbFormat<T>::value);
+      uint32_t pipe = 0;
+      uint32_t local = 0;
 #pragma unroll 1
-    for (int it = 0;; ++it) {
-      const int slot = it % kTileRing;
-      ptx::mbar_wait(&ti_full[slot], (it / kTileRing) & 1);
-      const int g = ti_item[slot];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&ti_empty[slot]);
-      if (g < 0) break;
-      const int kblocks = p.st[stage_of(p, g)].k_blocks;
-      const uint32_t acc = local & 1;
-      ptx::mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
-      ptx::tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-#pragma unroll 1
-      for (int kb = 0; kb < kblocks; ++kb, ++pipe) {
-        const int rs = pipe % S;
-        ptx::mbar_wait(&full[rs], (pipe / S) & 1);
+      for (int it = 0;; ++it) {
+        const int g = ring_take(it, false);
+        if (g < 0) break;
+        const int kblocks = p.st[stage_of(p, g)].k_blocks;
+        const uint32_t acc = local & 1;
+        if constexpr (CG == 2) {
+          ptx::mbar_wait_cluster(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
+        } else {
+          ptx::mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
+        }
         ptx::tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a_addr = ptx::smem_u32(sA + rs * C::kABytes);
-          const uint32_t b_addr = ptx::smem_u32(sB + rs * C::kBBytes);
+        const uint32_t d_tmem = tmem_base + acc * BN;
+#pragma unroll 1
+        for (int kb = 0; kb < kblocks; ++kb, ++pipe) {
+          const int rs = pipe % S;
+          ptx::mbar_wait(&full[rs], (pipe / S) & 1);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = ptx::smem_u32(sA + rs * C::kABytes);
+            const uint32_t b_addr = ptx::smem_u32(sB + rs * C::kBBytes);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            ptx::umma_f16(d_tmem, ptx::smem_desc_k_sw128(a_addr + k * 32),
-                          ptx::smem_desc_k_sw128(b_addr + k * 32), kIdesc, (kb | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t ad = ptx::smem_desc_k_sw128(a_addr + k * 32);
+              const uint64_t bd = ptx::smem_desc_k_sw128(b_addr + k * 32);
+              if constexpr (CG == 2) {
+                ptx::umma_f16_pair(d_tmem, ad, bd, kIdesc, (kb | k) != 0);
+              } else {
+                ptx::umma_f16(d_tmem, ad, bd, kIdesc, (kb | k) != 0);
+              }
+            }
+            if constexpr (CG == 2) {
+              ptx::umma_commit_pair(&empty[rs]);
+            } else {
+              ptx::umma_commit(&empty[rs]);
+            }
           }
-          ptx::umma_commit(&empty[rs]);
+          __syncwarp();
+        }
+        if (lane == 0) {
+          if constexpr (CG == 2) {
+            ptx::umma_commit_pair(&tmem_full[acc]);
+          } else {
+            ptx::umma_commit(&tmem_full[acc]);
+          }
         }
         __syncwarp();
+        ++local;
       }
-      if (lane == 0) ptx::umma_commit(&tmem_full[acc]);
-      __syncwarp();
-      ++local;
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int ew = warp - 4;  // == warp % 4: TMEM lanes [32*ew, 32*ew+32)
     uint32_t local = 0;
+    uint32_t tmem_empty_remote[2] = {0, 0}, peer_done_remote[2] = {0, 0};
+    if constexpr (CG == 2) {
+      if (!leader) {
+        for (int i = 0; i < 2; ++i) {
+          tmem_empty_remote[i] = ptx::mapa(&tmem_empty[i], 0);
+          peer_done_remote[i] = ptx::mapa(&peer_done[i], 0);
+        }
+      }
+    }
 #pragma unroll 1
     for (int it = 0;; ++it) {
-      const int slot = it % kTileRing;
-      ptx::mbar_wait(&ti_full[slot], (it / kTileRing) & 1);
-      const int g = ti_item[slot];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&ti_empty[slot]);
+      const int g = ring_take(it, CG == 2 && !leader);
       if (g < 0) break;
-      const int s = stage_of(p, g);
-      const StageParams& st = p.st[s];
-      const int tb = g - st.item_begin;
-      int tx, ty, tz;
-      order_tile(st.order, st.order_stride, Grid3{st.grid_x, st.grid_y, 1}, tb, &tx, &ty, &tz);
+      const Tile t = decode(p, g);
+      const StageParams& st = p.st[t.s];
       const uint32_t acc = local & 1;
-      ptx::mbar_wait(&tmem_full[acc], (local >> 1) & 1);
+      if constexpr (CG == 2) {
+        ptx::mbar_wait_cluster(&tmem_full[acc], (local >> 1) & 1);
+      } else {
+        ptx::mbar_wait(&tmem_full[acc], (local >> 1) & 1);
+      }
       ptx::tc_fence_after();
-      const int row = tx * kBM + ew * 32 + lane;
+      const int row = t.tx * C::kTileM + static_cast<int>(rank) * 128 + ew * 32 + lane;
       const bool row_ok = row < st.m;
       const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
       T* crow = reinterpret_cast<T*>(st.c) + static_cast<size_t>(row) * st.ldc;
       if (st.epilogue == TS_EPI_SWIGLU) {
-        T* out = crow + ty * (BN / 2);
+        T* out = crow + t.ty * (BN / 2);
 #pragma unroll 1
         for (int cc = 0; cc < BN / 64; ++cc) {
           uint32_t gr[32], ur[32];
@@ -349,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
           }
         }
       } else {
-        T* out = crow + ty * BN;
+        T* out = crow + t.ty * BN;
         const bool gelu = st.epilogue == TS_EPI_GELU;
 #pragma unroll 1
         for (int cc = 0; cc < BN / 32; ++cc) {
@@ -375,33 +490,52 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         }
       }
       ptx::tc_fence_before();
-      if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
-      // stage.post(): every epilogue thread's stores happen-before the release below.
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-      if (threadIdx.x == 128 && st.n_out_deps > 0) {
-        const uint64_t t = ptx::global_timer();
-        __threadfence();
-        ptx::fence_proxy_async_global();
-        for (int i = 0; i < st.n_out_deps; ++i) {
-          const int d = st.out_deps[i];
-          const DepParams& dp = p.dep[d];
-          const int idx = post_target(dp.policy, dp.param, tx, ty, Grid3{dp.pgx, dp.pgy, dp.pgz});
-          const int old = ptx::atom_add_release_gpu(dp.sem + idx, 1);
-          trace_event(p, t, 3, s, tb, -1, d, idx, old + 1, tx, ty);
+      if (lane == 0) {
+        if (CG == 2 && !leader) {
+          ptx::mbar_arrive_remote(tmem_empty_remote[acc]);
+        } else {
+          ptx::mbar_arrive(&tmem_empty[acc]);
         }
-        trace_event(p, t, 4, s, tb, -1, -1, -1, -1, tx, ty);
-      } else if (threadIdx.x == 128) {
-        trace_event(p, ptx::global_timer(), 4, s, tb, -1, -1, -1, -1, tx, ty);
+      }
+      // stage.post(): every epilogue thread's stores (of both CTAs of a pair)
+      // happen-before the release below.
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+      if (threadIdx.x == 128) {
+        if (CG == 2 && !leader) {
+          __threadfence();
+          ptx::mbar_arrive_remote(peer_done_remote[acc]);
+        } else {
+          if constexpr (CG == 2) ptx::mbar_wait_cluster(&peer_done[acc], (local >> 1) & 1);
+          const uint64_t tnow = ptx::global_timer();
+          if (st.n_out_deps > 0) {
+            __threadfence();
+            ptx::fence_proxy_async_global();
+            for (int i = 0; i < st.n_out_deps; ++i) {
+              const int d = st.out_deps[i];
+              const DepParams& dp = p.dep[d];
+              const int idx = post_target(dp.policy, dp.param, t.tx, t.ty,
+                                          Grid3{dp.pgx, dp.pgy, dp.pgz});
+              const int old = ptx::atom_add_release_gpu(dp.sem + idx, 1);
+              trace_event(p, tnow, 3, t.s, t.tb, -1, d, idx, old + 1, t.tx, t.ty);
+            }
+          }
+          trace_event(p, tnow, 4, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty);
+        }
       }
       ++local;
     }
   }
 
   // ---- teardown: free TMEM; the last CTA out restores the zero invariant -------------
-  __syncthreads();
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) {
+    ptx::cluster_sync();
+  } else {
+    __syncthreads();
+  }
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+    ptx::tmem_dealloc<C::kTmemCols, CG>(tmem_base);
   }
   if (threadIdx.x == 0) {
     __threadfence();

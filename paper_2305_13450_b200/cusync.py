@@ -77,7 +77,7 @@ class CuStage:
     @property
     def grid(self) -> Dim3:
         """Tile grid as the reference's Stage.grid sees it (row tiles, column tiles)."""
-        return Dim3(-(-self.m // BM), max(1, self.n // self.cs.tile_n), 1)
+        return Dim3(-(-self.m // self.cs.tile_m), max(1, self.n // self.cs.tile_n), 1)
 
     def flops(self) -> int:
         return 2 * self.m * self.n * self.k
@@ -101,11 +101,13 @@ class CuSync:
     """A chain of dependent GeMM stages launched through libtilesync_b200.so."""
 
     tile_n: int = 256
+    cta_group: int = 2
     mode: str = "fused"
     reorder: bool = True
     watchdog: bool = True
     keep_sems: bool = False
     num_ctas: int = 0
+    extra_flags: int = 0
     device: torch.device | None = None
     stages: list[CuStage] = field(default_factory=list)
     deps: list[CuDep] = field(default_factory=list)
@@ -115,10 +117,17 @@ class CuSync:
             raise ConfigError(f"mode must be 'fused' or 'stream', got {self.mode!r}")
         if self.tile_n not in (64, 128, 256):
             raise ConfigError(f"tile_n must be 64, 128 or 256, got {self.tile_n}")
+        if self.cta_group not in (1, 2) or (self.cta_group == 2 and self.tile_n == 64):
+            raise ConfigError(f"cta_group must be 1 or 2 (2 needs tile_n >= 128)")
         self._desc: _lib.ChainDesc | None = None
         self._scratch: torch.Tensor | None = None
         self._trace: torch.Tensor | None = None
         self._trace_cap = 0
+
+    @property
+    def tile_m(self) -> int:
+        """Rows of one tile: 128 per CTA, 256 for a CTA pair."""
+        return BM * self.cta_group
 
     # -- construction (PAPER.md:338-342) ---------------------------------------------
     def stage(self, a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, epilogue: str = "none",
@@ -203,9 +212,11 @@ class CuSync:
             dd.sem = dep.sem.data_ptr()
         d.mode = _lib.TS_MODE_FUSED if self.mode == "fused" else _lib.TS_MODE_STREAM
         d.tile_n = self.tile_n
+        d.cta_group = self.cta_group
         d.flags = ((0 if self.reorder else _lib.TS_FLAG_NO_REORDER)
                    | (0 if self.watchdog else _lib.TS_FLAG_NO_WATCHDOG)
-                   | (_lib.TS_FLAG_KEEP_SEMS if self.keep_sems else 0))
+                   | (_lib.TS_FLAG_KEEP_SEMS if self.keep_sems else 0)
+                   | self.extra_flags)
         d.num_ctas = self.num_ctas
         if self._scratch is None:
             self._scratch = torch.zeros(_lib.TS_SCRATCH_INTS, dtype=torch.int32,
