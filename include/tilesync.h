@@ -51,7 +51,9 @@ typedef enum {
 
 typedef enum {
   TS_ORDER_ROW_MAJOR = 0,        /* RowMajor        policies.py:56-58 */
-  TS_ORDER_STRIDED_ROW_MAJOR = 1 /* StridedRowMajor policies.py:61-70, param = stride */
+  TS_ORDER_STRIDED_ROW_MAJOR = 1, /* StridedRowMajor policies.py:61-70, param = stride */
+  TS_ORDER_BANDED_COLUMN_MAJOR = 2 /* extension: bands of `param` tile rows, column-major
+                                      inside a band (weight-block reuse in L2)        */
 } ts_order_kind;
 
 /* ---- host mirrors of the policy layer --------------------------------------------
@@ -165,7 +167,7 @@ typedef struct {
   int32_t value;     /* expected (wait_*) or post value (post), -1 = none */
   int16_t x, y;      /* tile coordinate */
   int16_t z, smid;   /* slice, SM id */
-  int32_t pad;
+  int32_t clk;       /* low 32 bits of the SM cycle counter (clock64) */
 } ts_trace_rec;
 
 /* Validate `desc` on the host and enqueue the chain on `stream`. Returns before the

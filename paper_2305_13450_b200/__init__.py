@@ -15,9 +15,10 @@ from .engine import (CostModel, Dependency, Event, Metrics, Mode, Scenario, SimO
 from .errors import ConfigError, MalformedTraceError
 from .gpu import (B200_SMS, Dim3, GpuConfig, TileCoord, WaveCount, linearize, tbs_per_wave,
                   utilization, waves)
-from .policies import (Conv2DTileSync, RowMajor, RowSync, SemaphoreArray, StridedRowMajor,
-                       StridedSync, SyncPolicy, TileOrder, TileSync, WaitSpec, check_policy,
-                       consumer_wait, is_sync, order_tile, post_target, sem_count, wait_steps)
+from .policies import (BandedColumnMajor, Conv2DTileSync, RowMajor, RowSync, SemaphoreArray,
+                       StridedRowMajor, StridedSync, SyncPolicy, TileOrder, TileSync, WaitSpec,
+                       check_policy, consumer_wait, is_sync, order_tile, post_target,
+                       sem_count, wait_steps)
 
 __version__ = "0.1.0"
 
@@ -28,7 +29,8 @@ __all__ = [
     "ConfigError", "MalformedTraceError",
     "B200_SMS", "Dim3", "GpuConfig", "TileCoord", "WaveCount", "linearize", "tbs_per_wave",
     "utilization", "waves",
-    "Conv2DTileSync", "RowMajor", "RowSync", "SemaphoreArray", "StridedRowMajor",
+    "BandedColumnMajor", "Conv2DTileSync", "RowMajor", "RowSync", "SemaphoreArray",
+    "StridedRowMajor",
     "StridedSync", "SyncPolicy", "TileOrder", "TileSync", "WaitSpec", "check_policy",
     "consumer_wait", "is_sync", "order_tile", "post_target", "sem_count", "wait_steps",
     "CuSync", "CuStage", "CuDep", "MlpChain", "SwigluChain", "interleave_gate_up", "mlp",

@@ -18,7 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libtilesync_b200.so"
 TS_OK, TS_ERR_CONFIG, TS_ERR_VALUE, TS_ERR_TYPE, TS_ERR_CUDA, TS_ERR_DEADLOCK = range(6)
 
 TS_POLICY_TILE, TS_POLICY_ROW, TS_POLICY_STRIDED, TS_POLICY_CONV2D = range(4)
-TS_ORDER_ROW_MAJOR, TS_ORDER_STRIDED_ROW_MAJOR = range(2)
+TS_ORDER_ROW_MAJOR, TS_ORDER_STRIDED_ROW_MAJOR, TS_ORDER_BANDED_COLUMN_MAJOR = range(3)
 TS_DTYPE_F16, TS_DTYPE_BF16 = range(2)
 TS_EPI_NONE, TS_EPI_GELU, TS_EPI_SWIGLU = range(3)
 TS_MODE_STREAM, TS_MODE_FUSED = range(2)
@@ -72,7 +72,7 @@ class TraceRec(ctypes.Structure):
         ("tb", ctypes.c_int32), ("k", ctypes.c_int32), ("dep", ctypes.c_int32),
         ("sem", ctypes.c_int32), ("value", ctypes.c_int32),
         ("x", ctypes.c_int16), ("y", ctypes.c_int16), ("z", ctypes.c_int16),
-        ("smid", ctypes.c_int16), ("pad", ctypes.c_int32),
+        ("smid", ctypes.c_int16), ("clk", ctypes.c_int32),
     ]
 
 

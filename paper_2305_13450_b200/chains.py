@@ -15,7 +15,7 @@ from __future__ import annotations
 import torch
 
 from .cusync import CuSync
-from .policies import RowSync, SyncPolicy
+from .policies import RowMajor, RowSync, SyncPolicy, TileOrder
 
 
 class MlpChain:
@@ -24,15 +24,16 @@ class MlpChain:
     def __init__(self, x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor,
                  policy: SyncPolicy = RowSync(), mode: str = "fused", tile_n: int = 256,
                  reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0,
-                 extra_flags: int = 0, cta_group: int = 2):
+                 extra_flags: int = 0, cta_group: int = 2, prod_order: TileOrder = RowMajor(),
+                 cons_order: TileOrder = RowMajor()):
         m = x.shape[0]
         self.x, self.w1, self.w2 = x, w1, w2
         self.h = torch.empty(m, w1.shape[0], dtype=x.dtype, device=x.device)
         self.y = torch.empty(m, w2.shape[0], dtype=x.dtype, device=x.device)
         self.cs = CuSync(tile_n=tile_n, mode=mode, reorder=reorder, keep_sems=keep_sems,
                          num_ctas=num_ctas, extra_flags=extra_flags, cta_group=cta_group)
-        self.prod = self.cs.stage(x, w1, self.h, epilogue="gelu", id="gemm1")
-        self.cons = self.cs.stage(self.h, w2, self.y, id="gemm2")
+        self.prod = self.cs.stage(x, w1, self.h, epilogue="gelu", order=prod_order, id="gemm1")
+        self.cons = self.cs.stage(self.h, w2, self.y, order=cons_order, id="gemm2")
         self.dep = self.cs.dependency(policy, self.prod, self.cons, operand="a")
 
     def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:

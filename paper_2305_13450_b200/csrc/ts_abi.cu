@@ -193,14 +193,17 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.ldc = st.ldc;
     sp.grid_x = (st.m + tile_m - 1) / tile_m;
     sp.grid_y = st.n / bn;
-    if (st.order != TS_ORDER_ROW_MAJOR && st.order != TS_ORDER_STRIDED_ROW_MAJOR)
+    if (st.order != TS_ORDER_ROW_MAJOR && st.order != TS_ORDER_STRIDED_ROW_MAJOR &&
+        st.order != TS_ORDER_BANDED_COLUMN_MAJOR)
       return fail(TS_ERR_TYPE, "stage %d: unknown order %d", s, st.order);
     if (st.order == TS_ORDER_STRIDED_ROW_MAJOR &&
         (st.order_stride < 1 || sp.grid_y % st.order_stride != 0))
       return fail(TS_ERR_CONFIG, "stage %d: order stride %d does not divide grid columns %d", s,
                   st.order_stride, sp.grid_y);
+    if (st.order == TS_ORDER_BANDED_COLUMN_MAJOR && st.order_stride < 1)
+      return fail(TS_ERR_CONFIG, "stage %d: band %d must be >= 1", s, st.order_stride);
     sp.order = st.order;
-    sp.order_stride = st.order == TS_ORDER_STRIDED_ROW_MAJOR ? st.order_stride : 1;
+    sp.order_stride = st.order == TS_ORDER_ROW_MAJOR ? 1 : st.order_stride;
     sp.epilogue = st.epilogue;
     sp.k_blocks = st.k / ts::kBK;
     sp.item_begin = items;
@@ -348,10 +351,12 @@ int ts_order_tile(int order, int stride, int gx, int gy, int gz, int counter, in
   const ts::Grid3 g{gx, gy, gz};
   if (counter < 0 || counter >= g.total())
     return fail(TS_ERR_VALUE, "counter %d outside grid %dx%dx%d", counter, gx, gy, gz);
-  if (order != ts::kRowMajor && order != ts::kStridedRowMajor)
+  if (order != ts::kRowMajor && order != ts::kStridedRowMajor && order != ts::kBandedColumnMajor)
     return fail(TS_ERR_TYPE, "unknown order %d", order);
   if (order == ts::kStridedRowMajor && (stride < 1 || gy % stride != 0))
     return fail(TS_ERR_CONFIG, "stride %d does not divide grid columns %d", stride, gy);
+  if (order == ts::kBandedColumnMajor && stride < 1)
+    return fail(TS_ERR_CONFIG, "band %d must be >= 1", stride);
   ts::order_tile(order, stride, g, counter, x, y, z);
   return TS_OK;
 }

@@ -120,7 +120,7 @@ __device__ __forceinline__ void trace_event(const ChainParams& p, uint64_t t, in
   r.y = static_cast<int16_t>(y);
   r.z = 0;
   r.smid = static_cast<int16_t>(ptx::sm_id());
-  r.pad = 0;
+  r.clk = static_cast<int32_t>(clock64());  // SM cycles, for per-tile frequency
   p.trace[slot] = r;
 }
 
@@ -315,6 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         const int d = st.in_dep;
         const int bh = b_hint ? b_hint : (st.grid_x == 1 ? 1 : 2);
         const uint64_t pol_b = bh == 1 ? pol_first : (bh == 2 ? pol_normal : pol_last);
+        const int ah = (p.flags >> 10) & 3;
+        const uint64_t pol_a = ah == 1 ? pol_first : (ah == 2 ? pol_normal : pol_last);
+        // diagnostic only (flag bit 12): time the chain without semaphore waits
+        const bool no_wait = (p.flags >> 12) & 1;
 #pragma unroll 1
         for (int kb = 0; kb < st.k_blocks; ++kb, ++pipe) {
           const int rs = pipe % S;
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
             }
           };
           if (reorder) load_b();
-          if (d >= 0) {
+          if (d >= 0 && !no_wait) {
             const DepParams& dp = p.dep[d];
             if (kb % dp.kb_per_kstep == 0) {
               const int kstep = kb / dp.kb_per_kstep;
@@ -347,9 +351,9 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
             }
           }
           if constexpr (CG == 2) {
-            ptx::tma_load_2d_pair(a_dst, &st.tmap_a, full_cluster[rs], kb * kBK, m0, pol_last);
+            ptx::tma_load_2d_pair(a_dst, &st.tmap_a, full_cluster[rs], kb * kBK, m0, pol_a);
           } else {
-            ptx::tma_load_2d(a_dst, &st.tmap_a, &full[rs], kb * kBK, m0, pol_last);
+            ptx::tma_load_2d(a_dst, &st.tmap_a, &full[rs], kb * kBK, m0, pol_a);
           }
           if (!reorder) load_b();
         }

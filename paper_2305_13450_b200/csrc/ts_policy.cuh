@@ -21,7 +21,7 @@
 namespace ts {
 
 enum PolicyKind : int { kTile = 0, kRow = 1, kStrided = 2, kConv2D = 3 };
-enum OrderKind : int { kRowMajor = 0, kStridedRowMajor = 1 };
+enum OrderKind : int { kRowMajor = 0, kStridedRowMajor = 1, kBandedColumnMajor = 2 };
 enum Status : int { kOk = 0, kConfig = 1, kValue = 2, kType = 3 };
 
 struct Grid3 {
@@ -119,12 +119,27 @@ TS_HD bool waits_at(int kind, int param, int k) {
 // order_tile — policies.py:181-205.  The tile of a stage's n-th counter draw.
 // Lexicographic (x, y, z) with z fastest; StridedRowMajor regroups the column axis so
 // that columns `stride` apart are drawn consecutively (group g = {g, g+s, g+2s, ...}).
+//
+// Extension (not in the reference simulator; the paper notes CuSync supports further
+// orders): BandedColumnMajor(band) walks bands of `band` tile rows in
+// order and, inside a band, goes column by column. Row-band tiles that read the same
+// weight column block are then in flight together, so the block streams from HBM once
+// per band instead of once per row; band = 1 is RowMajor.
 TS_HD void order_tile(int kind, int stride, Grid3 g, int n, int* x, int* y, int* z) {
   int zz = n % g.z;
   int rest = n / g.z;
+  *z = zz;
+  if (kind == kBandedColumnMajor) {
+    const int per_band = stride * g.y;
+    const int b = rest / per_band;
+    const int off = rest % per_band;
+    const int rows = (g.x - b * stride) < stride ? (g.x - b * stride) : stride;
+    *x = b * stride + off % rows;
+    *y = off / rows;
+    return;
+  }
   int pos = rest % g.y;  // position along the (possibly regrouped) column walk
   *x = rest / g.y;
-  *z = zz;
   if (kind == kStridedRowMajor) {
     int per_group = g.y / stride;
     *y = pos / per_group + (pos % per_group) * stride;

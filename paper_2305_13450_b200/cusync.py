@@ -266,15 +266,19 @@ class CuSync:
         for d in self.deps:
             d.sem.zero_()
 
-    def trace_events(self) -> list[Event]:
-        """The device trace as reference Events, times in ns from the first event."""
+    def trace_records(self) -> list:
+        """Raw device trace records (ts_trace_rec), in recording order."""
         if self._trace is None:
             raise RuntimeError("tracing is not enabled (call enable_trace() first)")
-        n = min(int(self._scratch[2].item()), self._trace_cap)
-        raw = self._trace[: n * _lib.TRACE_REC_BYTES].cpu().numpy().tobytes()
-        recs = (_lib.TraceRec * n).from_buffer_copy(raw) if n else []
-        if n and int(self._scratch[2].item()) > self._trace_cap:
+        count = int(self._scratch[2].item())
+        if count > self._trace_cap:
             raise RuntimeError("trace buffer overflowed")
+        raw = self._trace[: count * _lib.TRACE_REC_BYTES].cpu().numpy().tobytes()
+        return list((_lib.TraceRec * count).from_buffer_copy(raw)) if count else []
+
+    def trace_events(self) -> list[Event]:
+        """The device trace as reference Events, times in ns from the first event."""
+        recs = self.trace_records()
         t0 = min((r.t_ns for r in recs), default=0)
         dep_ids = [d.id for d in self.deps]
         evs = []

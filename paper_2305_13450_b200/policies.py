@@ -62,7 +62,17 @@ class StridedRowMajor:
     stride: int
 
 
-TileOrder = Union[RowMajor, StridedRowMajor]
+@dataclass(frozen=True)
+class BandedColumnMajor:
+    """Extension order (not in the reference simulator; the paper lists further orders,
+    PAPER.md:427): bands of `band` tile rows in order, column by column inside a band,
+    so the row tiles that share a weight column block run together and the block
+    streams from HBM once per band. ``BandedColumnMajor(1)`` is RowMajor."""
+
+    band: int
+
+
+TileOrder = Union[RowMajor, StridedRowMajor, BandedColumnMajor]
 
 
 @dataclass(frozen=True)
@@ -110,6 +120,8 @@ def order_code(order: TileOrder) -> tuple[int, int]:
         return _lib.TS_ORDER_ROW_MAJOR, 1
     if isinstance(order, StridedRowMajor):
         return _lib.TS_ORDER_STRIDED_ROW_MAJOR, order.stride
+    if isinstance(order, BandedColumnMajor):
+        return _lib.TS_ORDER_BANDED_COLUMN_MAJOR, order.band
     raise TypeError(f"unknown order {order!r}")
 
 

@@ -26,6 +26,20 @@ def summarize(cs, label):
             wb[key] += e.time - we[(key, e.k)]
     makespan = max(fin.values())
     print(f"== {label}: makespan {makespan / 1e3:.1f} us, events {len(evs)}")
+    # per-tile SM clock from (clock64, globaltimer) at claim and at finish (same CTA)
+    recs = cs.trace_records()
+    start = {(r.stage, r.tb): r for r in recs if r.kind == 0}
+    for s_i, st in enumerate(cs.stages):
+        mhz = []
+        for r in recs:
+            if r.kind == 4 and r.stage == s_i and (r.stage, r.tb) in start:
+                a = start[(r.stage, r.tb)]
+                if a.smid == r.smid and r.t_ns > a.t_ns:
+                    mhz.append(((r.clk - a.clk) % (1 << 32)) / (r.t_ns - a.t_ns) * 1e3)
+        if mhz:
+            mhz.sort()
+            print(f"  {st.id}: SM clock per tile median {mhz[len(mhz) // 2]:.0f} MHz "
+                  f"min {mhz[0]:.0f} max {mhz[-1]:.0f}")
     for st in cs.stages:
         d = [fin[k] - sched[k] for k in sched if k[0] == st.id]
         w = [wb[k] for k in sched if k[0] == st.id]
@@ -34,6 +48,15 @@ def summarize(cs, label):
         print(f"  {st.id}: tiles {len(d)} dur mean {sum(d) / len(d) / 1e3:.1f} us "
               f"min {min(d) / 1e3:.1f} max {max(d) / 1e3:.1f}; wait mean {sum(w) / len(w) / 1e3:.2f} us "
               f"max {max(w) / 1e3:.1f}; span {s0 / 1e3:.1f}..{f1 / 1e3:.1f} us")
+    if len(cs.stages) > 1:
+        p_end = max(fin[k] for k in fin if k[0] == cs.stages[0].id)
+        for name, sel in (("during producers", lambda k: sched[k] < p_end),
+                          ("after producers", lambda k: sched[k] >= p_end)):
+            ks = [k for k in sched if k[0] == cs.stages[1].id and sel(k)]
+            if ks:
+                d = sum(fin[k] - sched[k] - wb[k] for k in ks) / len(ks)
+                print(f"  {cs.stages[1].id} {name}: {len(ks)} tiles, mean busy (dur-wait) "
+                      f"{d / 1e3:.1f} us")
     # busy tiles over time (in 5% buckets)
     nb = 20
     busy = [0.0] * nb
@@ -45,20 +68,41 @@ def summarize(cs, label):
     print("  tiles in flight per 5% bucket:", " ".join(f"{b:.0f}" for b in busy))
 
 
+def order(s):
+    if s == "row":
+        return ts.RowMajor()
+    return ts.BandedColumnMajor(int(s[4:]))  # "band<N>"
+
+
 def main():
-    b, pol, tn = int(sys.argv[1]), sys.argv[2], int(sys.argv[3])
+    """argv: B then variants MODE:POLICY:PROD_ORDER:CONS_ORDER, e.g. fused:row:row:band4"""
+    b = int(sys.argv[1])
+    variants = sys.argv[2:] or ["stream:row:row:row", "fused:row:row:row"]
     torch.manual_seed(0)
     x = torch.randn(b, H, device="cuda").half()
     w1 = (torch.randn(H // 2, H, device="cuda") / H ** 0.5).half()
     w2 = (torch.randn(H, H // 2, device="cuda") / (H // 2) ** 0.5).half()
-    policy = {"row": ts.RowSync(), "tile": ts.TileSync()}[pol]
-    for mode in ("stream", "fused"):
-        ch = ts.MlpChain(x, w1, w2, policy=policy, mode=mode, tile_n=tn)
+    for v in variants:
+        parts = v.split(":")
+        mode, pol, po, co = parts[:4]
+        flags = int(parts[4], 0) if len(parts) > 4 else 0
+        policy = {"row": ts.RowSync(), "tile": ts.TileSync()}[pol]
+        ch = ts.MlpChain(x, w1, w2, policy=policy, mode=mode, prod_order=order(po),
+                         cons_order=order(co), extra_flags=flags)
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        for _ in range(3):
+            ch()
+        e0.record()
+        for _ in range(10):
+            ch()
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"-- {v}: untraced {e0.elapsed_time(e1) / 10 * 1e3:.1f} us/chain")
         ch.cs.enable_trace()
         for _ in range(3):
             ch()
         torch.cuda.synchronize()
-        summarize(ch.cs, f"B={b} {mode} {pol} tn={tn}")
+        summarize(ch.cs, f"B={b} {v}")
 
 
 if __name__ == "__main__":
