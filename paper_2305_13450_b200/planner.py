@@ -1,0 +1,99 @@
+"""Co-scheduling planner: pick the tile shape, CTA group, policy and tile orders of a
+chain from measured candidates on the device it will run on.
+
+The paper observes that no single policy wins everywhere; which one wins
+on B200 depends on wave quantization over 148 SMs, on HBM reuse of
+the weight panels and on the power cap. Rather than model all of that, the planner times
+a small candidate set with CUDA events (3 warm-up + 10 timed launches each) and keeps
+the fastest. ``wave_table`` gives the closed-form wave arithmetic the candidates come
+from (reference gpu.waves at GpuConfig(148)).
+"""
+
+from __future__ import annotations
+
+import itertools
+
+import torch
+
+from .chains import MlpChain
+from .gpu import GpuConfig, waves
+from .policies import BandedColumnMajor, RowMajor, RowSync, TileSync
+
+
+def _time(fn, iters=10, warm=3) -> float:
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / iters
+
+
+def candidates(m: int, mode: str):
+    out = []
+    for cg, tn in ((2, 256), (1, 256), (2, 128), (1, 128)):
+        gx = -(-m // (128 * cg))
+        orders = [RowMajor()] + ([BandedColumnMajor(gx)] if gx > 1 else [])
+        pols = [RowSync(), TileSync()] if mode == "fused" else [RowSync()]
+        for pol, co in itertools.product(pols, orders):
+            out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=cg, cons_order=co))
+    return out
+
+
+def describe(kw) -> dict:
+    co = kw.get("cons_order", RowMajor())
+    return {"mode": kw["mode"], "policy": type(kw["policy"]).__name__,
+            "tile": f"{128 * kw['cta_group']}x{kw['tile_n']}", "cta_group": kw["cta_group"],
+            "consumer_order": type(co).__name__ + (f"({co.band})" if hasattr(co, "band") else "")}
+
+
+def pick_mlp(x, w1, w2, mode="fused"):
+    """Time every candidate; return (best kwargs for MlpChain, [(desc, us), ...])."""
+    table = []
+    best, best_us = None, float("inf")
+    for kw in candidates(x.shape[0], mode):
+        ch = MlpChain(x, w1, w2, **kw)
+        us = _time(ch)
+        if ch.cs.watchdog_fired():
+            continue
+        table.append({**describe(kw), "us": us})
+        if us < best_us:
+            best, best_us = kw, us
+    return best, table
+
+
+def sweep_mlp(batches=(1, 64, 256, 512, 1024, 2048), hidden=12288, ffn=6144, device=None):
+    """GPT-3 MLP shard latency per batch: best fused, best stream-synced, cuBLAS."""
+    torch.manual_seed(7)
+    w1 = (torch.randn(ffn, hidden, device=device) / hidden ** 0.5).half()
+    w2 = (torch.randn(hidden, ffn, device=device) / ffn ** 0.5).half()
+    rows = []
+    for b in batches:
+        x = torch.randn(b, hidden, device=device).half()
+        fk, _ = pick_mlp(x, w1, w2, "fused")
+        sk, _ = pick_mlp(x, w1, w2, "stream")
+        fu = _time(MlpChain(x, w1, w2, **fk), iters=20)
+        su = _time(MlpChain(x, w1, w2, **sk), iters=20)
+        cu = _time(lambda: torch.nn.functional.gelu(x @ w1.t()) @ w2.t(), iters=20)
+        flops = 2 * b * hidden * ffn * 2
+        rows.append({"batch": b, "fused_us": fu, "stream_us": su, "cublas_us": cu,
+                     "speedup_vs_stream": su / fu, "speedup_vs_cublas": cu / fu,
+                     "fused_tflops": flops / fu / 1e6, "fused": describe(fk),
+                     "stream": describe(sk)})
+    return rows
+
+
+def wave_table(m: int, n1: int, n2: int, tile_m: int, tile_n: int, sms: int = 148):
+    """Stream vs fused whole-wave counts for the two GeMMs."""
+    units = sms // (tile_m // 128)
+    g = GpuConfig(units)
+    t1 = -(-m // tile_m) * (n1 // tile_n)
+    t2 = -(-m // tile_m) * (n2 // tile_n)
+    stream = waves(t1, g, 1).ceil + waves(t2, g, 1).ceil
+    fine = waves(t1 + t2, g, 1).ceil
+    return {"tiles": (t1, t2), "stream_waves": stream, "fine_waves": fine,
+            "bound": stream / fine}

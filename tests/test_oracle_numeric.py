@@ -1,0 +1,58 @@
+"""The oracle's numeric chain and its CPU protocol executor (test infrastructure).
+
+The reference has no numeric code, so the numeric restatement of
+PAPER.md:143-165 is cross-checked here against an independent float64 evaluation, and
+the CPU executor of the protocol against the plain chain and the closed-form final
+semaphores."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import tilesync_oracle as O
+
+
+def f64_mlp(x, w1, w2, dtype):
+    h = x.astype(np.float64) @ w1.astype(np.float64).T
+    h = 0.5 * h * (1 + np.vectorize(math.erf)(h / math.sqrt(2)))
+    h = O.round_to(h.astype(np.float32), dtype).astype(np.float64)
+    return h, h @ w2.astype(np.float64).T
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_mlp_chain_matches_float64(dtype):
+    rng = np.random.default_rng(0)
+    x = O.round_to(rng.standard_normal((40, 96), dtype=np.float32), dtype)
+    w1 = O.round_to(rng.standard_normal((64, 96), dtype=np.float32) / 10, dtype)
+    w2 = O.round_to(rng.standard_normal((32, 64), dtype=np.float32) / 8, dtype)
+    h, y = O.mlp_chain(x, w1, w2, dtype)
+    h64, y64 = f64_mlp(x, w1, w2, dtype)
+    # h is rounded to the storage dtype: allow one ulp flips from fp32 vs fp64 rounding
+    ulp = 2 ** -10 if dtype == "fp16" else 2 ** -7
+    assert np.all(np.abs(h - h64) <= ulp * np.maximum(np.abs(h64), 1e-3) + 1e-6)
+    assert np.allclose(y, y64, rtol=1e-3, atol=1e-3)
+
+
+def test_round_to_bf16_is_round_nearest_even():
+    v = np.array([1.0, 1.00390625, 1.01171875, -2.5, 3.0e38], dtype=np.float32)
+    r = O.round_to(v, "bf16")
+    assert r[0] == 1.0 and r[1] == 1.0 and r[2] == 1.015625 and r[3] == -2.5
+
+
+@pytest.mark.parametrize("policy", [(O.ROW, 0), (O.TILE, 0), (O.CONV2D, 1)])
+def test_cpu_protocol_executor(policy):
+    rng = np.random.default_rng(1)
+    m, k, n1, n2 = 300, 128, 256, 192
+    x = O.round_to(rng.standard_normal((m, k), dtype=np.float32), "fp16")
+    w1 = O.round_to(rng.standard_normal((n1, k), dtype=np.float32) / 11, "fp16")
+    w2 = O.round_to(rng.standard_normal((n2, n1), dtype=np.float32) / 16, "fp16")
+    h, y, sems = O.run_chain_cpu(x, w1, w2, tile_m=128, tile_n=64, policy=policy, threads=4)
+    h_ref, y_ref = O.mlp_chain(x, w1, w2, "fp16")
+    assert np.array_equal(h, h_ref)
+    assert np.allclose(y, y_ref, rtol=1e-4, atol=1e-4)
+    g1 = (3, 4, 1)
+    stages = [{"id": "p", "grid": g1, "k_steps": 4, "order": (O.ROW_MAJOR, 1)},
+              {"id": "c", "grid": (3, 3, 1), "k_steps": 4, "order": (O.ROW_MAJOR, 1)}]
+    deps = [{"producer": "p", "consumer": "c", "operand": "a", "policy": policy}]
+    assert sems == O.final_semaphores(stages, deps)["p->c/a"]
