@@ -158,7 +158,9 @@ typedef struct {
 /* Device trace record (one event of the reference's JSONL schema, engine.py:220-248). */
 typedef struct {
   uint64_t t_ns;     /* %globaltimer */
-  int32_t kind;      /* 0 scheduled, 1 wait_begin, 2 wait_end, 3 post, 4 finished */
+  int32_t kind;      /* 0 scheduled, 1 wait_begin, 2 wait_end, 3 post, 4 finished;
+                        extensions: 5 mma_begin, 6 mma_end (value = ns the tile's MMAs
+                        waited for operands after the first stage) */
   int32_t stage;     /* stage index */
   int32_t tb;        /* claim index within the stage (reference `tb`) */
   int32_t k;         /* reference k-step, -1 = none */

@@ -158,19 +158,23 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
 // the semaphores stay monotone as in SemaphoreArray, policies.py:84-99). Exponential
 // back-off keeps the polling traffic and issue slots of waiting SMs low.
 __device__ __forceinline__ void sem_wait(const ChainParams& p, const int* sem, int expected) {
-  if (ptx::ld_acquire_gpu(sem) >= expected) return;
-  const bool watchdog = (p.flags & TS_FLAG_NO_WATCHDOG) == 0;
-  uint64_t t0 = ptx::global_timer();
-  uint32_t ns = 32;
+  // Relaxed probes, then one acquire fence once the count is reached (an acquiring load
+  // per probe would invalidate L1 on every iteration).
+  if (ptx::ld_relaxed_gpu(sem) < expected) {
+    const bool watchdog = (p.flags & TS_FLAG_NO_WATCHDOG) == 0;
+    uint64_t t0 = ptx::global_timer();
+    uint32_t ns = 32;
 #pragma unroll 1
-  while (ptx::ld_acquire_gpu(sem) < expected) {
-    __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
-    if (watchdog && ptx::global_timer() - t0 > kWatchdogNs) {
-      atomicExch(&p.scratch[3], 1);
-      return;
+    while (ptx::ld_relaxed_gpu(sem) < expected) {
+      __nanosleep(ns);
+      if (ns < 256) ns <<= 1;
+      if (watchdog && ptx::global_timer() - t0 > kWatchdogNs) {
+        atomicExch(&p.scratch[3], 1);
+        break;
+      }
     }
   }
+  ptx::fence_acq_rel_gpu();
 }
 
 struct Tile {
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         const int slot = it % kTileRing;
         if (leader) {
           if constexpr (CG == 2) {
-            ptx::mbar_wait_cluster(&ti_empty[slot], ((it / kTileRing) & 1) ^ 1);
+            ptx::mbar_wait(&ti_empty[slot], ((it / kTileRing) & 1) ^ 1);  // no data: slot reuse
           } else {
             ptx::mbar_wait(&ti_empty[slot], ((it / kTileRing) & 1) ^ 1);
           }
@@ -372,16 +376,29 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         const int kblocks = p.st[stage_of(p, g)].k_blocks;
         const uint32_t acc = local & 1;
         if constexpr (CG == 2) {
-          ptx::mbar_wait_cluster(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
+          // TMEM reuse only; tcgen05 fences order the peer's loads before this MMA
+          ptx::mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
         } else {
           ptx::mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
         }
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+        const bool tr = p.trace != nullptr;
+        uint64_t starve_ns = 0;  // time this tile's MMAs waited for operand stages
 #pragma unroll 1
         for (int kb = 0; kb < kblocks; ++kb, ++pipe) {
           const int rs = pipe % S;
-          ptx::mbar_wait(&full[rs], (pipe / S) & 1);
+          if (tr && !ptx::mbar_try_wait(&full[rs], (pipe / S) & 1)) {
+            const uint64_t t0 = ptx::global_timer();
+            ptx::mbar_wait(&full[rs], (pipe / S) & 1);
+            if (kb > 0) starve_ns += ptx::global_timer() - t0;
+          } else {
+            ptx::mbar_wait(&full[rs], (pipe / S) & 1);
+          }
+          if (tr && kb == 0 && lane == 0) {
+            const Tile t = decode(p, g);
+            trace_event(p, ptx::global_timer(), 5, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty);
+          }
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint32_t a_addr = ptx::smem_u32(sA + rs * C::kABytes);
@@ -410,6 +427,12 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
           } else {
             ptx::umma_commit(&tmem_full[acc]);
           }
+          if (tr) {
+            const Tile t = decode(p, g);
+            trace_event(p, ptx::global_timer(), 6, t.s, t.tb, -1, -1, -1,
+                        static_cast<int>(starve_ns > 0x7fffffff ? 0x7fffffff : starve_ns), t.tx,
+                        t.ty);
+          }
         }
         __syncwarp();
         ++local;
@@ -436,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
       const StageParams& st = p.st[t.s];
       const uint32_t acc = local & 1;
       if constexpr (CG == 2) {
-        ptx::mbar_wait_cluster(&tmem_full[acc], (local >> 1) & 1);
+        ptx::mbar_wait(&tmem_full[acc], (local >> 1) & 1);  // arrived by the MMA commit
       } else {
         ptx::mbar_wait(&tmem_full[acc], (local >> 1) & 1);
       }

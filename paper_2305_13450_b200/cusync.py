@@ -231,7 +231,7 @@ class CuSync:
         if capacity is None:
             capacity = 0
             for st in self.stages:
-                capacity += st.grid.total() * (3 + 2 * 2 * max(1, st.k // BK))
+                capacity += st.grid.total() * (5 + 2 * 2 * max(1, st.k // BK))
         self._trace_cap = capacity
         self._trace = torch.zeros(capacity * _lib.TRACE_REC_BYTES, dtype=torch.uint8,
                                   device=self.device)
@@ -283,6 +283,8 @@ class CuSync:
         dep_ids = [d.id for d in self.deps]
         evs = []
         for i, r in enumerate(recs):
+            if r.kind >= len(_KINDS):
+                continue  # MMA-side extension records (see trace_records)
             kind = _KINDS[r.kind]
             ev = Event(time=int(r.t_ns - t0), stage=self.stages[r.stage].id, tb=r.tb, kind=kind,
                        tile=(r.x, r.y, r.z),

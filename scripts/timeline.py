@@ -48,6 +48,35 @@ def summarize(cs, label):
         print(f"  {st.id}: tiles {len(d)} dur mean {sum(d) / len(d) / 1e3:.1f} us "
               f"min {min(d) / 1e3:.1f} max {max(d) / 1e3:.1f}; wait mean {sum(w) / len(w) / 1e3:.2f} us "
               f"max {max(w) / 1e3:.1f}; span {s0 / 1e3:.1f}..{f1 / 1e3:.1f} us")
+    mb = {(r.stage, r.tb): r.t_ns for r in recs if r.kind == 5}
+    me = {(r.stage, r.tb): r for r in recs if r.kind == 6}
+    t0 = min(r.t_ns for r in recs)
+    for s_i, st in enumerate(cs.stages):
+        keys = [k for k in me if k[0] == s_i and k in mb and k in start]
+        if keys:
+            mma = [me[k].t_ns - mb[k] for k in keys]
+            starve = [me[k].value for k in keys]
+            lead = [mb[k] - start[k].t_ns for k in keys]
+            print(f"  {st.id}: MMA span mean {sum(mma) / len(mma) / 1e3:.1f} us, operand-starved "
+                  f"{sum(starve) / len(starve) / 1e3:.1f} us, claim->first MMA "
+                  f"{sum(lead) / len(lead) / 1e3:.1f} us")
+    # MMA idle per CTA(-pair leader): before its first tile, between tiles, after its last
+    per_sm = defaultdict(list)
+    for k, r in me.items():
+        if k in mb:
+            per_sm[r.smid].append((mb[k], r.t_ns))
+    if per_sm:
+        t_end = max(e for v in per_sm.values() for _, e in v)
+        head = gaps = tail = 0.0
+        for v in per_sm.values():
+            v.sort()
+            head += v[0][0] - t0
+            gaps += sum(max(0, v[i + 1][0] - v[i][1]) for i in range(len(v) - 1))
+            tail += t_end - v[-1][1]
+        n = len(per_sm)
+        print(f"  MMA idle per unit ({n} units): head {head / n / 1e3:.1f} us, between tiles "
+              f"{gaps / n / 1e3:.1f} us, tail {tail / n / 1e3:.1f} us "
+              f"(makespan {(t_end - t0) / 1e3:.1f} us)")
     if len(cs.stages) > 1:
         p_end = max(fin[k] for k in fin if k[0] == cs.stages[0].id)
         for name, sel in (("during producers", lambda k: sched[k] < p_end),
