@@ -126,6 +126,10 @@ typedef struct {
   int epilogue;  /* ts_epilogue */
   int order;     /* ts_order_kind */
   int order_stride;
+  int splits;        /* split-K slices (the reference's z extent); 0/1 = none.
+                        > 1 needs swap_ab, a workspace and counters */
+  float* workspace;  /* splits > 1: device fp32[tiles * splits * tile_n * 128]         */
+  int* counters;     /* splits > 1: device int32[tiles], zero on entry (kept zero)     */
 } ts_stage_desc;
 
 typedef struct {
@@ -144,6 +148,8 @@ typedef struct {
   int tile_n;    /* 64, 128 or 256; 0 = 256 */
   int cta_group; /* 1: one CTA per 128-row tile; 2: CTA pair per 256-row tile
                     (tcgen05 cta_group::2); 0 = 2 */
+  int swap_ab;   /* 1: small-batch tiles — UMMA M over 128 weight rows, UMMA N = tile_n
+                    (32/64/128/256) over activation rows; needs cta_group 1 */
   int flags;     /* ts_flags bitmask */
   int num_ctas;  /* persistent CTAs; 0 = one per SM */
   int* scratch;  /* device int32[TS_SCRATCH_INTS], zero on first use; kernels restore it */

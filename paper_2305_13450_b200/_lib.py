@@ -44,6 +44,8 @@ class StageDesc(ctypes.Structure):
         ("lda", ctypes.c_int), ("ldb", ctypes.c_int), ("ldc", ctypes.c_int),
         ("dtype", ctypes.c_int), ("epilogue", ctypes.c_int),
         ("order", ctypes.c_int), ("order_stride", ctypes.c_int),
+        ("splits", ctypes.c_int), ("workspace", ctypes.c_void_p),
+        ("counters", ctypes.c_void_p),
     ]
 
 
@@ -60,7 +62,7 @@ class ChainDesc(ctypes.Structure):
         ("n_stages", ctypes.c_int), ("stages", StageDesc * TS_MAX_STAGES),
         ("n_deps", ctypes.c_int), ("deps", DepDesc * TS_MAX_DEPS),
         ("mode", ctypes.c_int), ("tile_n", ctypes.c_int), ("cta_group", ctypes.c_int),
-        ("flags", ctypes.c_int),
+        ("swap_ab", ctypes.c_int), ("flags", ctypes.c_int),
         ("num_ctas", ctypes.c_int), ("scratch", ctypes.c_void_p),
         ("trace", ctypes.c_void_p), ("trace_cap", ctypes.c_int),
     ]

@@ -25,15 +25,19 @@ class MlpChain:
                  policy: SyncPolicy = RowSync(), mode: str = "fused", tile_n: int = 256,
                  reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0,
                  extra_flags: int = 0, cta_group: int = 2, prod_order: TileOrder = RowMajor(),
-                 cons_order: TileOrder = RowMajor()):
+                 cons_order: TileOrder = RowMajor(), swap_ab: bool = False,
+                 prod_splits: int = 1, cons_splits: int = 1):
         m = x.shape[0]
         self.x, self.w1, self.w2 = x, w1, w2
         self.h = torch.empty(m, w1.shape[0], dtype=x.dtype, device=x.device)
         self.y = torch.empty(m, w2.shape[0], dtype=x.dtype, device=x.device)
         self.cs = CuSync(tile_n=tile_n, mode=mode, reorder=reorder, keep_sems=keep_sems,
-                         num_ctas=num_ctas, extra_flags=extra_flags, cta_group=cta_group)
-        self.prod = self.cs.stage(x, w1, self.h, epilogue="gelu", order=prod_order, id="gemm1")
-        self.cons = self.cs.stage(self.h, w2, self.y, order=cons_order, id="gemm2")
+                         num_ctas=num_ctas, extra_flags=extra_flags, cta_group=cta_group,
+                         swap_ab=swap_ab)
+        self.prod = self.cs.stage(x, w1, self.h, epilogue="gelu", order=prod_order, id="gemm1",
+                                  splits=prod_splits)
+        self.cons = self.cs.stage(self.h, w2, self.y, order=cons_order, id="gemm2",
+                                  splits=cons_splits)
         self.dep = self.cs.dependency(policy, self.prod, self.cons, operand="a")
 
     def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:

@@ -81,13 +81,13 @@ int sm_count() {
 }
 
 // `units` = tiles in flight at once (CTAs for CG=1, CTA pairs for CG=2).
-template <int BN, int CG, typename T>
+template <int BN, int CG, typename T, bool SW = false>
 int launch_one(const ts::ChainParams& p, int units, cudaStream_t stream) {
-  using C = ts::Cfg<BN, CG>;
+  using C = ts::Cfg<BN, CG, SW>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(ts::chain_kernel<BN, CG, T>,
+    attr_err = cudaFuncSetAttribute(ts::chain_kernel<BN, CG, T, SW>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   });
   if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
@@ -103,7 +103,7 @@ int launch_one(const ts::ChainParams& p, int units, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, ts::chain_kernel<BN, CG, T>, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, ts::chain_kernel<BN, CG, T, SW>, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "chain_kernel launch");
   return TS_OK;
@@ -119,8 +119,23 @@ int launch_bn(int bn, const ts::ChainParams& p, int units, cudaStream_t s) {
   return fail(TS_ERR_VALUE, "tile_n must be 64, 128 or 256 (got %d)", bn);
 }
 
-int launch_dispatch(int bn, int cg, int dtype, const ts::ChainParams& p, int units,
+template <typename T>
+int launch_swapped(int bn, const ts::ChainParams& p, int units, cudaStream_t s) {
+  switch (bn) {
+    case 32: return launch_one<32, 1, T, true>(p, units, s);
+    case 64: return launch_one<64, 1, T, true>(p, units, s);
+    case 128: return launch_one<128, 1, T, true>(p, units, s);
+    case 256: return launch_one<256, 1, T, true>(p, units, s);
+  }
+  return fail(TS_ERR_VALUE, "swapped tile_n must be 32, 64, 128 or 256 (got %d)", bn);
+}
+
+int launch_dispatch(int bn, int cg, int swap, int dtype, const ts::ChainParams& p, int units,
                     cudaStream_t s) {
+  if (swap) {
+    return dtype == TS_DTYPE_BF16 ? launch_swapped<__nv_bfloat16>(bn, p, units, s)
+                                  : launch_swapped<__half>(bn, p, units, s);
+  }
   if (cg == 2) {
     if (bn == 64) return fail(TS_ERR_VALUE, "cta_group 2 needs tile_n >= 128");
     return dtype == TS_DTYPE_BF16 ? launch_bn<2, __nv_bfloat16>(bn, p, units, s)
@@ -131,11 +146,15 @@ int launch_dispatch(int bn, int cg, int dtype, const ts::ChainParams& p, int uni
 }
 
 int tile_n_of(const ts_chain_desc* d) { return d->tile_n == 0 ? 256 : d->tile_n; }
-int cta_group_of(const ts_chain_desc* d) { return d->cta_group == 0 ? 2 : d->cta_group; }
+int cta_group_of(const ts_chain_desc* d) {
+  if (d->swap_ab) return 1;
+  return d->cta_group == 0 ? 2 : d->cta_group;
+}
 
 // Output columns one tile of stage `st` writes (the producer "column tile" width that a
 // consumer k-step covers).
-int out_tile_cols(const ts_stage_desc& st, int bn) {
+int out_tile_cols(const ts_stage_desc& st, int bn, int swap) {
+  if (swap) return 128;
   return st.epilogue == TS_EPI_SWIGLU ? bn / 2 : bn;
 }
 
@@ -144,12 +163,20 @@ int out_tile_cols(const ts_stage_desc& st, int bn) {
 int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
   if (d == nullptr) return fail(TS_ERR_VALUE, "null chain descriptor");
   const int bn = tile_n_of(d);
-  if (bn != 64 && bn != 128 && bn != 256)
+  const int swap = d->swap_ab ? 1 : 0;
+  if (swap) {
+    if (bn != 32 && bn != 64 && bn != 128 && bn != 256)
+      return fail(TS_ERR_VALUE, "swapped tile_n must be 32, 64, 128 or 256 (got %d)", d->tile_n);
+    if (d->cta_group == 2) return fail(TS_ERR_VALUE, "swap_ab tiles use cta_group 1");
+  } else if (bn != 64 && bn != 128 && bn != 256) {
     return fail(TS_ERR_VALUE, "tile_n must be 64, 128 or 256 (got %d)", d->tile_n);
+  }
   const int cg = cta_group_of(d);
   if (cg != 1 && cg != 2) return fail(TS_ERR_VALUE, "cta_group must be 1 or 2 (got %d)", d->cta_group);
   if (cg == 2 && bn == 64) return fail(TS_ERR_VALUE, "cta_group 2 needs tile_n >= 128");
-  const int tile_m = 128 * cg;
+  // reference-grid tile: rows of activations x columns of output
+  const int tile_m = swap ? bn : 128 * cg;
+  const int tile_n = swap ? 128 : bn;
   if (d->n_stages < 1 || d->n_stages > TS_MAX_STAGES)
     return fail(TS_ERR_CONFIG, "n_stages must be in [1, %d]", TS_MAX_STAGES);
   if (d->n_deps < 0 || d->n_deps > TS_MAX_DEPS)
@@ -173,12 +200,21 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     if (st.dtype != dtype) return fail(TS_ERR_CONFIG, "stage %d: all stages must share a dtype", s);
     if (st.epilogue < TS_EPI_NONE || st.epilogue > TS_EPI_SWIGLU)
       return fail(TS_ERR_TYPE, "stage %d: unknown epilogue %d", s, st.epilogue);
+    if (swap && st.epilogue == TS_EPI_SWIGLU)
+      return fail(TS_ERR_CONFIG, "stage %d: the SwiGLU epilogue needs the normal tile layout", s);
     if (st.m < 1 || st.n < 1 || st.k < 1)
       return fail(TS_ERR_VALUE, "stage %d: m, n, k must be >= 1", s);
-    if (st.n % bn != 0)
-      return fail(TS_ERR_CONFIG, "stage %d: n=%d is not a multiple of tile_n=%d", s, st.n, bn);
-    if (st.k % ts::kBK != 0)
-      return fail(TS_ERR_CONFIG, "stage %d: k=%d is not a multiple of %d", s, st.k, ts::kBK);
+    if (st.n % tile_n != 0)
+      return fail(TS_ERR_CONFIG, "stage %d: n=%d is not a multiple of the tile width %d", s, st.n,
+                  tile_n);
+    const int splits = st.splits < 1 ? 1 : st.splits;
+    if (st.k % (ts::kBK * splits) != 0)
+      return fail(TS_ERR_CONFIG, "stage %d: k=%d is not a multiple of %d x %d split(s)", s, st.k,
+                  ts::kBK, splits);
+    if (splits > 1 && !swap)
+      return fail(TS_ERR_CONFIG, "stage %d: split-K needs swap_ab tiles", s);
+    if (splits > 1 && (st.workspace == nullptr || st.counters == nullptr))
+      return fail(TS_ERR_VALUE, "stage %d: split-K needs a workspace and counters", s);
     const int n_out = st.epilogue == TS_EPI_SWIGLU ? st.n / 2 : st.n;
     if (st.lda < st.k || st.ldb < st.k || st.ldc < n_out || st.lda % 8 || st.ldb % 8 || st.ldc % 8)
       return fail(TS_ERR_VALUE, "stage %d: leading dimensions must cover the rows and be multiples of 8", s);
@@ -192,7 +228,10 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.k = st.k;
     sp.ldc = st.ldc;
     sp.grid_x = (st.m + tile_m - 1) / tile_m;
-    sp.grid_y = st.n / bn;
+    sp.grid_y = st.n / tile_n;
+    sp.splits = splits;
+    sp.ws = st.workspace;
+    sp.cnt = st.counters;
     if (st.order != TS_ORDER_ROW_MAJOR && st.order != TS_ORDER_STRIDED_ROW_MAJOR &&
         st.order != TS_ORDER_BANDED_COLUMN_MAJOR)
       return fail(TS_ERR_TYPE, "stage %d: unknown order %d", s, st.order);
@@ -207,14 +246,16 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.epilogue = st.epilogue;
     sp.k_blocks = st.k / ts::kBK;
     sp.item_begin = items;
-    items += sp.grid_x * sp.grid_y;
+    items += sp.grid_x * sp.grid_y * splits;
     sp.item_end = items;
     sp.in_dep = -1;
     sp.n_out_deps = 0;
     if (with_tmaps) {
-      int r = make_tmap(&sp.tmap_a, st.a, st.m, st.k, st.lda, st.dtype, 128);
+      // activations: box rows = 128 per CTA (normal) or tile_n (swapped);
+      // weights: box rows = tile_n / cta_group (normal) or 128 (swapped)
+      int r = make_tmap(&sp.tmap_a, st.a, st.m, st.k, st.lda, st.dtype, swap ? bn : 128);
       if (r) return r;
-      r = make_tmap(&sp.tmap_b, st.b, st.n, st.k, st.ldb, st.dtype, bn / cg);
+      r = make_tmap(&sp.tmap_b, st.b, st.n, st.k, st.ldb, st.dtype, swap ? 128 : bn / cg);
       if (r) return r;
     }
   }
@@ -231,7 +272,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       return fail(TS_ERR_CONFIG, "dependency %d: GeMM stages only consume operand A", i);
     const ts::StageParams& ps = p->st[dd.producer];
     ts::StageParams& cs = p->st[dd.consumer];
-    const ts::Grid3 pg{ps.grid_x, ps.grid_y, 1};
+    const ts::Grid3 pg{ps.grid_x, ps.grid_y, ps.splits};
     int r = ts::policy_check(dd.policy, dd.param, pg);
     if (r == ts::kType) return fail(TS_ERR_TYPE, "dependency %d: unknown policy %d", i, dd.policy);
     if (r) return fail(TS_ERR_CONFIG, "dependency %d: policy parameter %d invalid for producer grid %dx%d", i, dd.param, pg.x, pg.y);
@@ -240,10 +281,10 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
                   cs.grid_x, ps.grid_x);
     if (cs.in_dep >= 0)
       return fail(TS_ERR_CONFIG, "dependency %d: stage %d already has an operand-A dependency", i, dd.consumer);
-    const int cols = out_tile_cols(d->stages[dd.producer], bn);
-    if (d->stages[dd.consumer].k != ps.n / bn * cols)
+    const int cols = out_tile_cols(d->stages[dd.producer], bn, swap);
+    if (d->stages[dd.consumer].k != ps.grid_y * cols)
       return fail(TS_ERR_CONFIG, "dependency %d: consumer k=%d must equal producer output columns %d", i,
-                  d->stages[dd.consumer].k, ps.n / bn * cols);
+                  d->stages[dd.consumer].k, ps.grid_y * cols);
     int kb_per_kstep = cols / ts::kBK;
     int k_steps = cs.k_blocks / kb_per_kstep;
     if (dd.policy == ts::kConv2D) {
@@ -262,7 +303,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     dp.param = dd.param;
     dp.pgx = pg.x;
     dp.pgy = pg.y;
-    dp.pgz = 1;
+    dp.pgz = pg.z;
     dp.kb_per_kstep = kb_per_kstep;
     dp.sem_n = ts::sem_count(dd.policy, dd.param, pg);
     cs.in_dep = i;
@@ -394,7 +435,7 @@ int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
     p.item_lo = 0;
     p.item_hi = p.total_items;
     int grid = ctas < p.total_items ? ctas : p.total_items;
-    return launch_dispatch(bn, cg, dtype, p, grid, s);
+    return launch_dispatch(bn, cg, desc->swap_ab, dtype, p, grid, s);
   }
   // Stream mode: the same kernel, one launch per stage, no semaphores — the
   // stream-synchronized baseline (reference Mode.STREAM engine.py:40-42).
@@ -408,7 +449,7 @@ int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
     q.item_lo = q.st[i].item_begin;
     q.item_hi = q.st[i].item_end;
     const int n = q.item_hi - q.item_lo;
-    r = launch_dispatch(bn, cg, dtype, q, ctas < n ? ctas : n, s);
+    r = launch_dispatch(bn, cg, desc->swap_ab, dtype, q, ctas < n ? ctas : n, s);
     if (r) return r;
   }
   return TS_OK;

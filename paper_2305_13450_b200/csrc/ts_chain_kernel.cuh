@@ -43,14 +43,17 @@ constexpr int kEpiThreads = 128;
 constexpr uint64_t kWatchdogNs = 4000000000ull;
 
 struct StageParams {
-  CUtensorMap tmap_a;  // [m, k] K-major, box {64, 128}, 128-B swizzle
-  CUtensorMap tmap_b;  // [n, k] K-major, box {64, BN/CG}, 128-B swizzle
+  CUtensorMap tmap_a;  // activations [m, k] K-major, 128-B swizzle
+  CUtensorMap tmap_b;  // weights [n, k] K-major, 128-B swizzle
   void* c;
   int m, n, k, ldc;
   int grid_x, grid_y;
   int order, order_stride;
   int epilogue;
   int k_blocks;
+  int splits;    // split-K slices (the reference's z extent), >= 1
+  float* ws;     // splits > 1: fp32 partial tiles [tiles][splits][BN][128]
+  int* cnt;      // splits > 1: per-tile arrival counters (zero on entry and exit)
   int item_begin, item_end;
   int in_dep;  // dependency feeding operand A, or -1
   int n_out_deps;
@@ -76,16 +79,27 @@ struct ChainParams {
   int flags;
 };
 
-template <int BN, int CG>
+// Tile geometry. Normal layout: UMMA M runs over activation rows (128 per CTA, 256 per
+// CTA pair) and UMMA N = BN over weight rows. Swapped layout (SW, small batch): UMMA M
+// runs over 128 weight rows and UMMA N = BN over activation rows, so every in-flight
+// smem byte of the dominant operand is weight — the HBM-bound regime.
+template <int BN, int CG, bool SW = false>
 struct Cfg {
-  static constexpr int kTileM = 128 * CG;            // rows of a (pair) tile
-  static constexpr int kBRows = BN / CG;             // B rows each CTA loads
-  static constexpr int kABytes = 128 * kBK * 2;
-  static constexpr int kBBytes = kBRows * kBK * 2;
+  static constexpr int kTileM = SW ? BN : 128 * CG;  // activation rows of a tile
+  static constexpr int kTileN = SW ? 128 : BN;       // output columns of a tile
+  static constexpr int kBRows = SW ? BN : BN / CG;   // rows of the UMMA-N operand per CTA
+  static constexpr int kABytes = 128 * kBK * 2;      // UMMA-M operand stage
+  static constexpr int kBBytes = kBRows * kBK * 2;   // UMMA-N operand stage
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kTmemCols = 2 * BN;           // two accumulator buffers
+  static constexpr int kStagesMax = SW ? 12 : 8;
+  static constexpr int kStages = kStagesRaw > kStagesMax ? kStagesMax : kStagesRaw;
+  // Narrow swapped MMAs (128 x BN x 16, BN <= 64) are latency-bound when every one
+  // accumulates into the same TMEM region; rotating over kAcc independent accumulators
+  // (summed in the epilogue) keeps the tensor pipe busy.
+  static constexpr int kAcc = SW ? (BN >= 256 ? 1 : 256 / BN > 8 ? 8 : 256 / BN) : 1;
+  static constexpr int kAccCols = kAcc * BN;           // TMEM columns of one tile buffer
+  static constexpr int kTmemCols = 2 * kAccCols;       // two tile buffers
   static constexpr int kBarOffset = kStages * kStageBytes;
   // full, empty per stage; tmem full/empty x2; tile ring full/empty; peer_done x2
   static constexpr int kNumBars = 2 * kStages + 4 + 2 * kTileRing + 2;
@@ -103,7 +117,7 @@ __device__ __forceinline__ int stage_of(const ChainParams& p, int g) {
 
 __device__ __forceinline__ void trace_event(const ChainParams& p, uint64_t t, int kind,
                                             int stage, int tb, int k, int dep, int sem,
-                                            int value, int x, int y) {
+                                            int value, int x, int y, int z = 0) {
   if (p.trace == nullptr) return;
   int slot = atomicAdd(&p.scratch[2], 1);
   if (slot >= p.trace_cap) return;
@@ -118,7 +132,7 @@ __device__ __forceinline__ void trace_event(const ChainParams& p, uint64_t t, in
   r.value = value;
   r.x = static_cast<int16_t>(x);
   r.y = static_cast<int16_t>(y);
-  r.z = 0;
+  r.z = static_cast<int16_t>(z);
   r.smid = static_cast<int16_t>(ptx::sm_id());
   r.clk = static_cast<int32_t>(clock64());  // SM cycles, for per-tile frequency
   p.trace[slot] = r;
@@ -140,6 +154,17 @@ __device__ __forceinline__ float gelu_erf(float x) {
 }
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+template <typename T>
+__device__ __forceinline__ T to_elem(float v);
+template <>
+__device__ __forceinline__ __half to_elem<__half>(float v) {
+  return __float2half_rn(v);
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 to_elem<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
 
 template <typename T>
 __device__ __forceinline__ uint32_t pack2(float a, float b);
@@ -178,7 +203,7 @@ __device__ __forceinline__ void sem_wait(const ChainParams& p, const int* sem, i
 }
 
 struct Tile {
-  int g, s, tb, tx, ty;
+  int g, s, tb, tx, ty, tz;
 };
 
 __device__ __forceinline__ Tile decode(const ChainParams& p, int g) {
@@ -187,14 +212,15 @@ __device__ __forceinline__ Tile decode(const ChainParams& p, int g) {
   t.s = stage_of(p, g);
   const StageParams& st = p.st[t.s];
   t.tb = g - st.item_begin;
-  int tz;
-  order_tile(st.order, st.order_stride, Grid3{st.grid_x, st.grid_y, 1}, t.tb, &t.tx, &t.ty, &tz);
+  order_tile(st.order, st.order_stride, Grid3{st.grid_x, st.grid_y, st.splits}, t.tb, &t.tx,
+             &t.ty, &t.tz);
   return t;
 }
 
-template <int BN, int CG, typename T>
+template <int BN, int CG, typename T, bool SW>
 __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constant__ ChainParams p) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, SW>;
+  static_assert(!SW || CG == 1, "swapped tiles use single-CTA MMAs");
   constexpr int S = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -212,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
   int* ti_item = reinterpret_cast<int*>(peer_done + 2);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ti_item + kTileRing);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  int* split_flag = last_flag + 1;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -313,9 +340,11 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         if (g < 0) break;
         const Tile t = decode(p, g);
         const StageParams& st = p.st[t.s];
-        if (leader) trace_event(p, ptx::global_timer(), 0, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty);
-        const int m0 = t.tx * C::kTileM + static_cast<int>(rank) * 128;
-        const int n0 = t.ty * BN + static_cast<int>(rank) * C::kBRows;
+        if (leader)
+          trace_event(p, ptx::global_timer(), 0, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
+        // activation (dependent) and weight (independent) tile rows of this CTA
+        const int act_row = SW ? t.tx * BN : t.tx * C::kTileM + static_cast<int>(rank) * 128;
+        const int w_row = SW ? t.ty * 128 : t.ty * BN + static_cast<int>(rank) * C::kBRows;
         const int d = st.in_dep;
         const int bh = b_hint ? b_hint : (st.grid_x == 1 ? 1 : 2);
         const uint64_t pol_b = bh == 1 ? pol_first : (bh == 2 ? pol_normal : pol_last);
@@ -323,57 +352,93 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         const uint64_t pol_a = ah == 1 ? pol_first : (ah == 2 ? pol_normal : pol_last);
         // diagnostic only (flag bit 12): time the chain without semaphore waits
         const bool no_wait = (p.flags >> 12) & 1;
+        const int k_per = st.k_blocks / st.splits;  // K-blocks of this split-K slice
+        const int kb_begin = t.tz * k_per;
+        const int kb_end = kb_begin + k_per;
+        // stage.wait() for reference k-step `ks` (policies.py:145-166)
+        auto wait_kstep = [&](int ks) {
+          const DepParams& dp = p.dep[d];
+          Wait w = consumer_wait(dp.policy, dp.param, t.tx, t.ty, ks,
+                                 Grid3{dp.pgx, dp.pgy, dp.pgz}, dp.pgz);
+          if (w.sem < 0) return;
+          if (leader)
+            trace_event(p, ptx::global_timer(), 1, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
+                        t.ty, t.tz);
+          sem_wait(p, dp.sem + w.sem, w.expected);
+          if (leader)
+            trace_event(p, ptx::global_timer(), 2, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
+                        t.ty, t.tz);
+          ptx::fence_proxy_async_global();
+        };
+        const bool waits = d >= 0 && !no_wait;
+        const int kbpk = waits ? p.dep[d].kb_per_kstep : 1;
+        // K-loop rotation. At small batch every tile reads the same few activation lines
+        // for a given K-block; if all tiles walked K in the same order they would hit one
+        // L2 line at a time (measured: 1.9 TB/s instead of 6.4). Starting each weight
+        // column block at a different K-block spreads those reads while tiles sharing a
+        // weight block (same ty) stay in lockstep for L2 reuse. Allowed when the policy
+        // has no k-step ordering to respect (no dependency, or a single wait at k-step 0).
+        const bool ordered = waits && !(p.dep[d].policy == kRow || p.dep[d].policy == kStrided);
+        const int rot = (ordered || (p.flags >> 14) & 1) ? 0 : (t.ty * 37 + 5) % k_per;
+        if (waits && rot != 0) {
+          // every wait of the slice (only k-step 0 waits for Row/Strided) before any load
+          for (int ks = 0; ks * kbpk < st.k_blocks; ++ks) wait_kstep(ks);
+        } else if (waits) {
+          // A split-K slice of a consumer still performs every k-step's wait of the
+          // reference model (each z-slice of a tile runs all k-steps, engine.py:469-514):
+          // the ones before its K range up front (they cover the k-step it starts in) ...
+          for (int ks = 0; ks * kbpk < kb_begin; ++ks) wait_kstep(ks);
+        }
 #pragma unroll 1
-        for (int kb = 0; kb < st.k_blocks; ++kb, ++pipe) {
+        for (int i = 0; i < k_per; ++i, ++pipe) {
+          const int kb = kb_begin + (i + rot) % k_per;
           const int rs = pipe % S;
           ptx::mbar_wait(&empty[rs], ((pipe / S) & 1) ^ 1);
-          if (leader) ptx::mbar_arrive_expect_tx(&full[rs], CG * C::kStageBytes);
-          uint8_t* a_dst = sA + rs * C::kABytes;
-          uint8_t* b_dst = sB + rs * C::kBBytes;
+          // diagnostic only (flag bit 15): stream the weights, skip the activation loads
+          const bool skip_act = (p.flags >> 15) & 1;
+          if (leader)
+            ptx::mbar_arrive_expect_tx(&full[rs],
+                                       CG * (skip_act ? (SW ? C::kABytes : C::kBBytes)
+                                                      : C::kStageBytes));
+          // normal layout: activations -> UMMA-M operand (sA), weights -> UMMA-N (sB);
+          // swapped layout: weights -> sA, activations -> sB
+          uint8_t* act_dst = SW ? sB + rs * C::kBBytes : sA + rs * C::kABytes;
+          uint8_t* w_dst = SW ? sA + rs * C::kABytes : sB + rs * C::kBBytes;
           auto load_b = [&]() {
             if constexpr (CG == 2) {
-              ptx::tma_load_2d_pair(b_dst, &st.tmap_b, full_cluster[rs], kb * kBK, n0, pol_b);
+              ptx::tma_load_2d_pair(w_dst, &st.tmap_b, full_cluster[rs], kb * kBK, w_row, pol_b);
             } else {
-              ptx::tma_load_2d(b_dst, &st.tmap_b, &full[rs], kb * kBK, n0, pol_b);
+              ptx::tma_load_2d(w_dst, &st.tmap_b, &full[rs], kb * kBK, w_row, pol_b);
             }
           };
           if (reorder) load_b();
-          if (d >= 0 && !no_wait) {
-            const DepParams& dp = p.dep[d];
-            if (kb % dp.kb_per_kstep == 0) {
-              const int kstep = kb / dp.kb_per_kstep;
-              Wait w = consumer_wait(dp.policy, dp.param, t.tx, t.ty, kstep,
-                                     Grid3{dp.pgx, dp.pgy, dp.pgz}, dp.pgz);
-              if (w.sem >= 0) {
-                if (leader)
-                  trace_event(p, ptx::global_timer(), 1, t.s, t.tb, kstep, d, w.sem, w.expected, t.tx, t.ty);
-                sem_wait(p, dp.sem + w.sem, w.expected);
-                if (leader)
-                  trace_event(p, ptx::global_timer(), 2, t.s, t.tb, kstep, d, w.sem, w.expected, t.tx, t.ty);
-                ptx::fence_proxy_async_global();
-              }
-            }
-          }
-          if constexpr (CG == 2) {
-            ptx::tma_load_2d_pair(a_dst, &st.tmap_a, full_cluster[rs], kb * kBK, m0, pol_a);
+          if (waits && rot == 0 && kb % kbpk == 0) wait_kstep(kb / kbpk);
+          if (skip_act) {
+          } else if constexpr (CG == 2) {
+            ptx::tma_load_2d_pair(act_dst, &st.tmap_a, full_cluster[rs], kb * kBK, act_row, pol_a);
           } else {
-            ptx::tma_load_2d(a_dst, &st.tmap_a, &full[rs], kb * kBK, m0, pol_a);
+            ptx::tma_load_2d(act_dst, &st.tmap_a, &full[rs], kb * kBK, act_row, pol_a);
           }
           if (!reorder) load_b();
         }
+        // ... and the ones after it once its loads are issued.
+        if (waits && rot == 0)
+          for (int ks = (kb_end + kbpk - 1) / kbpk; ks * kbpk < st.k_blocks; ++ks) wait_kstep(ks);
       }
     }
   } else if (warp == 1) {
     // ===================== tcgen05.mma issuer (leader) =====================
     if (leader) {
-      constexpr uint32_t kIdesc = ptx::idesc_f16(C::kTileM, BN, AbFormat<T>::value);
+      // UMMA shape: M = 128 per CTA (256 for a pair), N = BN in both layouts
+      constexpr uint32_t kIdesc = ptx::idesc_f16(128 * CG, BN, AbFormat<T>::value);
       uint32_t pipe = 0;
       uint32_t local = 0;
 #pragma unroll 1
       for (int it = 0;; ++it) {
         const int g = ring_take(it, false);
         if (g < 0) break;
-        const int kblocks = p.st[stage_of(p, g)].k_blocks;
+        const StageParams& sp = p.st[stage_of(p, g)];
+        const int kblocks = sp.k_blocks / sp.splits;
         const uint32_t acc = local & 1;
         if constexpr (CG == 2) {
           // TMEM reuse only; tcgen05 fences order the peer's loads before this MMA
@@ -382,13 +447,13 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
           ptx::mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
         }
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
         const bool tr = p.trace != nullptr;
         uint64_t starve_ns = 0;  // time this tile's MMAs waited for operand stages
 #pragma unroll 1
         for (int kb = 0; kb < kblocks; ++kb, ++pipe) {
           const int rs = pipe % S;
-          if (tr && !ptx::mbar_try_wait(&full[rs], (pipe / S) & 1)) {
+          if (tr && !ptx::mbar_test_wait(&full[rs], (pipe / S) & 1)) {
             const uint64_t t0 = ptx::global_timer();
             ptx::mbar_wait(&full[rs], (pipe / S) & 1);
             if (kb > 0) starve_ns += ptx::global_timer() - t0;
@@ -400,6 +465,11 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
             trace_event(p, ptx::global_timer(), 5, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty);
           }
           ptx::tc_fence_after();
+          if ((p.flags >> 13) & 1) {  // diagnostic only: stream operands, skip the MMAs
+            if (lane == 0) ptx::mbar_arrive(&empty[rs]);
+            __syncwarp();
+            continue;
+          }
           if (lane == 0) {
             const uint32_t a_addr = ptx::smem_u32(sA + rs * C::kABytes);
             const uint32_t b_addr = ptx::smem_u32(sB + rs * C::kBBytes);
@@ -409,6 +479,10 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
               const uint64_t bd = ptx::smem_desc_k_sw128(b_addr + k * 32);
               if constexpr (CG == 2) {
                 ptx::umma_f16_pair(d_tmem, ad, bd, kIdesc, (kb | k) != 0);
+              } else if constexpr (C::kAcc > 1) {
+                const int step = kb * (kBK / 16) + k;  // rotate independent accumulators
+                ptx::umma_f16(d_tmem + (step % C::kAcc) * BN, ad, bd, kIdesc,
+                              step >= C::kAcc);
               } else {
                 ptx::umma_f16(d_tmem, ad, bd, kIdesc, (kb | k) != 0);
               }
@@ -464,9 +538,112 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         ptx::mbar_wait(&tmem_full[acc], (local >> 1) & 1);
       }
       ptx::tc_fence_after();
+      const uint32_t t_lane =
+          tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * C::kAccCols;
+      auto release_tmem = [&]() {
+        ptx::tc_fence_before();
+        if (lane == 0) {
+          if (CG == 2 && !leader) {
+            ptx::mbar_arrive_remote(tmem_empty_remote[acc]);
+          } else {
+            ptx::mbar_arrive(&tmem_empty[acc]);
+          }
+        }
+      };
+      if constexpr (SW) {
+        // Swapped tile: TMEM lane = output column, TMEM column = activation row.
+        const int ncl = ew * 32 + lane;
+        const int ncol = t.ty * 128 + ncl;
+        const int b0 = t.tx * BN;
+        const int rows = st.m - b0 < BN ? st.m - b0 : BN;
+        const bool gelu = st.epilogue == TS_EPI_GELU;
+        T* cout = reinterpret_cast<T*>(st.c) + ncol;
+        // accumulators the MMA warp actually wrote (fewer than kAcc for very short K)
+        const int steps = (st.k_blocks / st.splits) * (kBK / 16);
+        const int n_acc = steps < C::kAcc ? steps : C::kAcc;
+        // 32 activation rows [col, col+32) of this thread's output column, summed over the
+        // rotating accumulators
+        auto load_sum = [&](int col, float (&v)[32]) {
+          uint32_t r[32];
+          ptx::tmem_ld_32x32b_x32(t_lane + col, r);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+#pragma unroll 1
+          for (int a = 1; a < n_acc; ++a) {
+            ptx::tmem_ld_32x32b_x32(t_lane + a * BN + col, r);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += __uint_as_float(r[j]);
+          }
+        };
+        if (st.splits == 1) {
+#pragma unroll 1
+          for (int cc = 0; cc < BN / 32; ++cc) {
+            float v[32];
+            load_sum(cc * 32, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int b = cc * 32 + j;
+              const float o = gelu ? gelu_erf(v[j]) : v[j];
+              if (b < rows) cout[static_cast<size_t>(b0 + b) * st.ldc] = to_elem<T>(o);
+            }
+          }
+          release_tmem();
+        } else {
+          // Split-K slice (reference z > 1): publish the fp32 partial, count arrivals;
+          // the last slice to arrive sums all partials, applies the epilogue, stores.
+          const int tile_id = t.tx * st.grid_y + t.ty;
+          float* part = st.ws + (static_cast<size_t>(tile_id) * st.splits + t.tz) * BN * 128;
+#pragma unroll 1
+          for (int cc = 0; cc < BN / 32; ++cc) {
+            float v[32];
+            load_sum(cc * 32, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (cc * 32 + j < rows) part[(cc * 32 + j) * 128 + ncl] = v[j];
+            }
+          }
+          release_tmem();
+          __threadfence();
+          asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+          if (threadIdx.x == 128) {
+            const int old = atomicAdd(&st.cnt[tile_id], 1);
+            *split_flag = (old == st.splits - 1);
+            if (old == st.splits - 1) st.cnt[tile_id] = 0;  // restore the zero invariant
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+          if (*split_flag) {
+            ptx::fence_acq_rel_gpu();
+            const float* base = st.ws + static_cast<size_t>(tile_id) * st.splits * BN * 128;
+            // 8 activation rows at a time so 8 x splits L2 loads are in flight together
+#pragma unroll 1
+            for (int b8 = 0; b8 < rows; b8 += 8) {
+              float s[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) s[j] = 0.f;
+#pragma unroll 1
+              for (int z = 0; z < st.splits; ++z) {
+                const float* src = base + (static_cast<size_t>(z) * BN + b8) * 128 + ncl;
+                float v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = b8 + j < rows ? __ldcg(src + j * 128) : 0.f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) s[j] += v[j];
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (b8 + j < rows) {
+                  const float o = gelu ? gelu_erf(s[j]) : s[j];
+                  cout[static_cast<size_t>(b0 + b8 + j) * st.ldc] = to_elem<T>(o);
+                }
+              }
+            }
+          }
+        }
+      } else {
       const int row = t.tx * C::kTileM + static_cast<int>(rank) * 128 + ew * 32 + lane;
       const bool row_ok = row < st.m;
-      const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
       T* crow = reinterpret_cast<T*>(st.c) + static_cast<size_t>(row) * st.ldc;
       if (st.epilogue == TS_EPI_SWIGLU) {
         T* out = crow + t.ty * (BN / 2);
@@ -516,14 +693,8 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
           }
         }
       }
-      ptx::tc_fence_before();
-      if (lane == 0) {
-        if (CG == 2 && !leader) {
-          ptx::mbar_arrive_remote(tmem_empty_remote[acc]);
-        } else {
-          ptx::mbar_arrive(&tmem_empty[acc]);
-        }
-      }
+      release_tmem();
+      }  // normal layout
       // stage.post(): every epilogue thread's stores (of both CTAs of a pair)
       // happen-before the release below.
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
@@ -543,10 +714,10 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
               const int idx = post_target(dp.policy, dp.param, t.tx, t.ty,
                                           Grid3{dp.pgx, dp.pgy, dp.pgz});
               const int old = ptx::atom_add_release_gpu(dp.sem + idx, 1);
-              trace_event(p, tnow, 3, t.s, t.tb, -1, d, idx, old + 1, t.tx, t.ty);
+              trace_event(p, tnow, 3, t.s, t.tb, -1, d, idx, old + 1, t.tx, t.ty, t.tz);
             }
           }
-          trace_event(p, tnow, 4, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty);
+          trace_event(p, tnow, 4, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
         }
       }
       ++local;

@@ -57,6 +57,9 @@ class CuStage:
     c: torch.Tensor
     epilogue: str
     order: TileOrder
+    splits: int = 1
+    ws: torch.Tensor | None = None
+    cnt: torch.Tensor | None = None
 
     @property
     def m(self) -> int:
@@ -72,12 +75,17 @@ class CuStage:
 
     @property
     def out_tile_cols(self) -> int:
+        """Output columns one tile writes (a consumer k-step in reference units)."""
+        if self.cs.swap_ab:
+            return 128
         return self.cs.tile_n // 2 if self.epilogue == "swiglu" else self.cs.tile_n
 
     @property
     def grid(self) -> Dim3:
-        """Tile grid as the reference's Stage.grid sees it (row tiles, column tiles)."""
-        return Dim3(-(-self.m // self.cs.tile_m), max(1, self.n // self.cs.tile_n), 1)
+        """Tile grid as the reference's Stage.grid sees it: (activation-row tiles,
+        output-column tiles, split-K slices)."""
+        cols = 128 if self.cs.swap_ab else self.cs.tile_n
+        return Dim3(-(-self.m // self.cs.tile_m), max(1, self.n // cols), self.splits)
 
     def flops(self) -> int:
         return 2 * self.m * self.n * self.k
@@ -108,6 +116,7 @@ class CuSync:
     keep_sems: bool = False
     num_ctas: int = 0
     extra_flags: int = 0
+    swap_ab: bool = False
     device: torch.device | None = None
     stages: list[CuStage] = field(default_factory=list)
     deps: list[CuDep] = field(default_factory=list)
@@ -115,10 +124,14 @@ class CuSync:
     def __post_init__(self) -> None:
         if self.mode not in ("fused", "stream"):
             raise ConfigError(f"mode must be 'fused' or 'stream', got {self.mode!r}")
-        if self.tile_n not in (64, 128, 256):
+        if self.swap_ab:
+            if self.tile_n not in (32, 64, 128, 256):
+                raise ConfigError(f"swapped tile_n must be 32, 64, 128 or 256, got {self.tile_n}")
+            self.cta_group = 1
+        elif self.tile_n not in (64, 128, 256):
             raise ConfigError(f"tile_n must be 64, 128 or 256, got {self.tile_n}")
         if self.cta_group not in (1, 2) or (self.cta_group == 2 and self.tile_n == 64):
-            raise ConfigError(f"cta_group must be 1 or 2 (2 needs tile_n >= 128)")
+            raise ConfigError("cta_group must be 1 or 2 (2 needs tile_n >= 128)")
         self._desc: _lib.ChainDesc | None = None
         self._scratch: torch.Tensor | None = None
         self._trace: torch.Tensor | None = None
@@ -126,12 +139,16 @@ class CuSync:
 
     @property
     def tile_m(self) -> int:
-        """Rows of one tile: 128 per CTA, 256 for a CTA pair."""
-        return BM * self.cta_group
+        """Activation rows of one tile: 128 per CTA, 256 for a CTA pair, tile_n when
+        swapped."""
+        return self.tile_n if self.swap_ab else BM * self.cta_group
 
     # -- construction (PAPER.md:338-342) ---------------------------------------------
     def stage(self, a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, epilogue: str = "none",
-              order: TileOrder = RowMajor(), id: str | None = None) -> CuStage:
+              order: TileOrder = RowMajor(), id: str | None = None,
+              splits: int = 1) -> CuStage:
+        """Add a GeMM stage. ``splits`` > 1 splits K into that many slices (the
+        reference's z extent): each slice posts once, consumers wait for all of them."""
         if len(self.stages) >= _lib.TS_MAX_STAGES:
             raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
         if epilogue not in _EPI:
@@ -148,8 +165,15 @@ class CuSync:
         n_out = b.shape[0] // 2 if epilogue == "swiglu" else b.shape[0]
         if c.shape[0] != a.shape[0] or c.shape[1] != n_out:
             raise ValueError(f"c must be [{a.shape[0]}, {n_out}], got {tuple(c.shape)}")
+        if splits < 1:
+            raise ConfigError("splits must be >= 1")
         st = CuStage(self, len(self.stages), id or f"gemm{len(self.stages) + 1}", a, b, c,
-                     epilogue, order)
+                     epilogue, order, splits)
+        if splits > 1:
+            tiles = st.grid.x * st.grid.y
+            st.ws = torch.empty(tiles * splits * self.tile_n * 128, dtype=torch.float32,
+                                device=a.device)
+            st.cnt = torch.zeros(tiles, dtype=torch.int32, device=a.device)
         self.stages.append(st)
         self.device = a.device
         self._desc = None
@@ -201,6 +225,9 @@ class CuSync:
             sd.dtype = _DT[st.a.dtype]
             sd.epilogue = _EPI[st.epilogue]
             sd.order, sd.order_stride = order_code(st.order)
+            sd.splits = st.splits
+            sd.workspace = st.ws.data_ptr() if st.ws is not None else None
+            sd.counters = st.cnt.data_ptr() if st.cnt is not None else None
         d.n_deps = len(self.deps)
         for i, dep in enumerate(self.deps):
             dd = d.deps[i]
@@ -213,6 +240,7 @@ class CuSync:
         d.mode = _lib.TS_MODE_FUSED if self.mode == "fused" else _lib.TS_MODE_STREAM
         d.tile_n = self.tile_n
         d.cta_group = self.cta_group
+        d.swap_ab = 1 if self.swap_ab else 0
         d.flags = ((0 if self.reorder else _lib.TS_FLAG_NO_REORDER)
                    | (0 if self.watchdog else _lib.TS_FLAG_NO_WATCHDOG)
                    | (_lib.TS_FLAG_KEEP_SEMS if self.keep_sems else 0)

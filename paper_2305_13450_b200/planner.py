@@ -34,11 +34,24 @@ def _time(fn, iters=10, warm=3) -> float:
 
 
 def candidates(m: int, mode: str):
+    """Candidate chain configurations for `m` activation rows.
+
+    Large batch: normal tiles (activations on the UMMA M side), CTA pairs or single CTAs,
+    RowMajor or band-ordered consumers. Small batch (m <= 256, HBM-bound on weights):
+    swapped tiles (weights on the UMMA M side, activations as UMMA N = the smallest tile
+    width >= m) with split-K slices so every SM streams weights.
+    """
     out = []
+    pols = [RowSync(), TileSync()] if mode == "fused" else [RowSync()]
+    if m <= 256:
+        tn = next(t for t in (32, 64, 128, 256) if t >= m)
+        for z1, z2 in ((3, 1), (3, 2), (2, 2), (2, 1), (1, 1)):
+            for pol in pols:
+                out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=1, swap_ab=True,
+                                prod_splits=z1, cons_splits=z2))
     for cg, tn in ((2, 256), (1, 256), (2, 128), (1, 128)):
         gx = -(-m // (128 * cg))
         orders = [RowMajor()] + ([BandedColumnMajor(gx)] if gx > 1 else [])
-        pols = [RowSync(), TileSync()] if mode == "fused" else [RowSync()]
         for pol, co in itertools.product(pols, orders):
             out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=cg, cons_order=co))
     return out
@@ -46,8 +59,13 @@ def candidates(m: int, mode: str):
 
 def describe(kw) -> dict:
     co = kw.get("cons_order", RowMajor())
-    return {"mode": kw["mode"], "policy": type(kw["policy"]).__name__,
-            "tile": f"{128 * kw['cta_group']}x{kw['tile_n']}", "cta_group": kw["cta_group"],
+    swap = kw.get("swap_ab", False)
+    tile = f"128x{kw['tile_n']}" if not swap else f"{kw['tile_n']}x128 (swapped)"
+    if not swap:
+        tile = f"{128 * kw['cta_group']}x{kw['tile_n']}"
+    return {"mode": kw["mode"], "policy": type(kw["policy"]).__name__, "tile": tile,
+            "cta_group": kw["cta_group"], "swap_ab": swap,
+            "splits": [kw.get("prod_splits", 1), kw.get("cons_splits", 1)],
             "consumer_order": type(co).__name__ + (f"({co.band})" if hasattr(co, "band") else "")}
 
 

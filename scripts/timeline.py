@@ -115,9 +115,12 @@ def main():
         parts = v.split(":")
         mode, pol, po, co = parts[:4]
         flags = int(parts[4], 0) if len(parts) > 4 else 0
+        swap_tn = int(parts[5]) if len(parts) > 5 else 0
+        splits = int(parts[6]) if len(parts) > 6 else 1
         policy = {"row": ts.RowSync(), "tile": ts.TileSync()}[pol]
+        kw = dict(swap_ab=True, tile_n=swap_tn, prod_splits=splits) if swap_tn else {}
         ch = ts.MlpChain(x, w1, w2, policy=policy, mode=mode, prod_order=order(po),
-                         cons_order=order(co), extra_flags=flags)
+                         cons_order=order(co), extra_flags=flags, **kw)
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         for _ in range(3):
             ch()
