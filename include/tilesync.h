@@ -130,7 +130,16 @@ typedef struct {
                         > 1 needs swap_ab, a workspace and counters */
   float* workspace;  /* splits > 1: device fp32[tiles * splits * tile_n * 128]         */
   int* counters;     /* splits > 1: device int32[tiles], zero on entry (kept zero)     */
+  int kind;          /* ts_stage_kind */
 } ts_stage_desc;
+
+typedef enum {
+  TS_STAGE_GEMM = 0,    /* C = epi(A x B^T) on tcgen05                                    */
+  TS_STAGE_ATTN_DOT = 1 /* attention's fused dot: a = XQKV [m, 3n] with
+                           [Q heads | K heads | V heads] 128-column head tiles, c = XDot
+                           [m, n]; XDot = Softmax(Q*V)*K per head and row (column-tile
+                           local, dropout p = 0); b unused. Tile = rows x one head.     */
+} ts_stage_kind;
 
 typedef struct {
   int producer, consumer; /* stage indices, producer < consumer                 */

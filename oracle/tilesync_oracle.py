@@ -280,6 +280,28 @@ def mlp_chain(x, w1, w2, dtype="fp16"):
     return h, h @ w2.astype(np.float32).T
 
 
+def attention_dot(qkv, heads, dtype="fp16"):
+    """The paper's fused dot, column-tile local as its StridedSync
+    dependency defines it: per row and 128-wide head, softmax(q*v) * k (dropout p=0)."""
+    m = qkv.shape[0]
+    q = qkv[:, : heads * 128].reshape(m, heads, 128).astype(np.float32)
+    k = qkv[:, heads * 128: 2 * heads * 128].reshape(m, heads, 128).astype(np.float32)
+    v = qkv[:, 2 * heads * 128:].reshape(m, heads, 128).astype(np.float32)
+    s = q * v
+    s = s - s.max(axis=2, keepdims=True)
+    p = np.exp(s)
+    p = p / p.sum(axis=2, keepdims=True)
+    return round_to((p * k).reshape(m, heads * 128), dtype)
+
+
+def attention_chain(x, w_qkv, w2, dtype="fp16"):
+    """XQKV = X Wqkv^T (rounded) -> XDot -> Y = XDot W2^T."""
+    qkv = round_to(x.astype(np.float32) @ w_qkv.astype(np.float32).T, dtype)
+    heads = w_qkv.shape[0] // (3 * 128)
+    dot = attention_dot(qkv, heads, dtype)
+    return qkv, dot, dot @ w2.astype(np.float32).T
+
+
 def swiglu_chain(x, w_gate, w_up, w_down, dtype="bf16"):
     g = x.astype(np.float32) @ w_gate.astype(np.float32).T
     u = x.astype(np.float32) @ w_up.astype(np.float32).T

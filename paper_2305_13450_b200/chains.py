@@ -83,3 +83,41 @@ class SwigluChain:
     def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         self.cs.launch(stream)
         return self.y
+
+
+class AttentionChain:
+    """GPT-3 self-attention block of the paper, TP-sharded:
+    XQKV = X @ Wqkv^T -> XDot = Dropout(Softmax(XQ . XV)) . XK -> Y = XDot @ W2^T.
+
+    Wqkv rows are [Q heads | K heads | V heads] with 128-wide heads (12 heads per rank
+    at TP=8). The QKV GeMM draws its tiles in StridedRowMajor(heads) order so the three
+    tiles of one head finish together (the paper's prodOrder); the dot
+    waits on StridedSync(heads) (one semaphore per row and head, expected 3); the output
+    GeMM consumes the dot's head tiles under `second_policy` (TileSync in the paper).
+    """
+
+    def __init__(self, x: torch.Tensor, w_qkv: torch.Tensor, w2: torch.Tensor,
+                 second_policy: SyncPolicy | None = None, mode: str = "fused",
+                 cta_group: int = 2, keep_sems: bool = False, num_ctas: int = 0,
+                 extra_flags: int = 0):
+        from .policies import StridedRowMajor, StridedSync, TileSync
+        m = x.shape[0]
+        n3 = w_qkv.shape[0]
+        if n3 % (3 * 128):
+            raise ValueError("Wqkv rows must be 3 x heads x 128")
+        heads = n3 // (3 * 128)
+        self.heads = heads
+        self.qkv = torch.empty(m, n3, dtype=x.dtype, device=x.device)
+        self.dot = torch.empty(m, n3 // 3, dtype=x.dtype, device=x.device)
+        self.y = torch.empty(m, w2.shape[0], dtype=x.dtype, device=x.device)
+        self.cs = CuSync(tile_n=128, mode=mode, cta_group=cta_group, keep_sems=keep_sems,
+                         num_ctas=num_ctas, extra_flags=extra_flags)
+        self.s_qkv = self.cs.stage(x, w_qkv, self.qkv, order=StridedRowMajor(heads), id="qkv")
+        self.s_dot = self.cs.stage_dot(self.qkv, self.dot, id="dot")
+        self.s_out = self.cs.stage(self.dot, w2, self.y, id="out")
+        self.cs.dependency(StridedSync(heads), self.s_qkv, self.s_dot, operand="qkv")
+        self.cs.dependency(second_policy or TileSync(), self.s_dot, self.s_out, operand="a")
+
+    def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        self.cs.launch(stream)
+        return self.y

@@ -198,6 +198,39 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     if (st.dtype != TS_DTYPE_F16 && st.dtype != TS_DTYPE_BF16)
       return fail(TS_ERR_TYPE, "stage %d: unknown dtype %d", s, st.dtype);
     if (st.dtype != dtype) return fail(TS_ERR_CONFIG, "stage %d: all stages must share a dtype", s);
+    if (st.kind == TS_STAGE_ATTN_DOT) {
+      if (swap) return fail(TS_ERR_CONFIG, "stage %d: the attention dot stage needs normal tiles", s);
+      if (st.m < 1 || st.n < 128 || st.n % 128)
+        return fail(TS_ERR_CONFIG, "stage %d: dot width %d must be a positive multiple of 128", s, st.n);
+      if (st.lda < 3 * st.n || st.lda % 8 || st.ldc < st.n || st.ldc % 8)
+        return fail(TS_ERR_VALUE, "stage %d: dot needs lda >= 3n and ldc >= n (multiples of 8)", s);
+      if (!st.a || !st.c) return fail(TS_ERR_VALUE, "stage %d: null operand pointer", s);
+      if ((reinterpret_cast<uintptr_t>(st.a) | reinterpret_cast<uintptr_t>(st.c)) & 15)
+        return fail(TS_ERR_VALUE, "stage %d: operands must be 16-byte aligned", s);
+      if (st.order != TS_ORDER_ROW_MAJOR && st.order != TS_ORDER_BANDED_COLUMN_MAJOR)
+        return fail(TS_ERR_CONFIG, "stage %d: unsupported order for the dot stage", s);
+      sp.kind = ts::kStageDot;
+      sp.a = st.a;
+      sp.lda = st.lda;
+      sp.c = st.c;
+      sp.m = st.m;
+      sp.n = st.n;
+      sp.ldc = st.ldc;
+      sp.grid_x = (st.m + tile_m - 1) / tile_m;
+      sp.grid_y = st.n / 128;
+      sp.splits = 1;
+      sp.order = st.order;
+      sp.order_stride = st.order == TS_ORDER_ROW_MAJOR ? 1 : (st.order_stride < 1 ? 1 : st.order_stride);
+      sp.epilogue = TS_EPI_NONE;
+      sp.item_begin = items;
+      items += sp.grid_x * sp.grid_y;
+      sp.item_end = items;
+      sp.in_dep = -1;
+      sp.n_out_deps = 0;
+      continue;
+    }
+    if (st.kind != TS_STAGE_GEMM) return fail(TS_ERR_TYPE, "stage %d: unknown stage kind %d", s, st.kind);
+    sp.kind = ts::kStageGemm;
     if (st.epilogue < TS_EPI_NONE || st.epilogue > TS_EPI_SWIGLU)
       return fail(TS_ERR_TYPE, "stage %d: unknown epilogue %d", s, st.epilogue);
     if (swap && st.epilogue == TS_EPI_SWIGLU)
@@ -281,12 +314,22 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
                   cs.grid_x, ps.grid_x);
     if (cs.in_dep >= 0)
       return fail(TS_ERR_CONFIG, "dependency %d: stage %d already has an operand-A dependency", i, dd.consumer);
-    const int cols = out_tile_cols(d->stages[dd.producer], bn, swap);
-    if (d->stages[dd.consumer].k != ps.grid_y * cols)
-      return fail(TS_ERR_CONFIG, "dependency %d: consumer k=%d must equal producer output columns %d", i,
-                  d->stages[dd.consumer].k, ps.grid_y * cols);
+    const int cols = ps.kind == ts::kStageDot ? 128 : out_tile_cols(d->stages[dd.producer], bn, swap);
     int kb_per_kstep = cols / ts::kBK;
-    int k_steps = cs.k_blocks / kb_per_kstep;
+    int k_steps = 0;
+    if (cs.kind == ts::kStageDot) {
+      // the dot reads [Q | K | V] = the producer's whole output row; one wait, k-step 0
+      if (d->stages[dd.consumer].a != d->stages[dd.producer].c ||
+          ps.grid_y * cols != 3 * cs.n)
+        return fail(TS_ERR_CONFIG, "dependency %d: the dot stage must read its producer's [m, 3n] output", i);
+      kb_per_kstep = 1;
+      k_steps = 1;
+    } else {
+      if (d->stages[dd.consumer].k != ps.grid_y * cols)
+        return fail(TS_ERR_CONFIG, "dependency %d: consumer k=%d must equal producer output columns %d", i,
+                    d->stages[dd.consumer].k, ps.grid_y * cols);
+      k_steps = cs.k_blocks / kb_per_kstep;
+    }
     if (dd.policy == ts::kConv2D) {
       if (kb_per_kstep % dd.param != 0)
         return fail(TS_ERR_CONFIG, "dependency %d: kk=%d does not divide the %d K-blocks of a producer tile", i, dd.param, kb_per_kstep);

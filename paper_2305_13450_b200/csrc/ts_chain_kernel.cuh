@@ -41,6 +41,8 @@ constexpr int kThreads = 256;
 constexpr int kTileRing = 4;    // tile-id hand-off ring between scheduler and consumers
 constexpr int kEpiThreads = 128;
 constexpr uint64_t kWatchdogNs = 4000000000ull;
+constexpr int kStageGemm = 0;  // C = epi(A x B^T) on tcgen05
+constexpr int kStageDot = 1;   // attention's fused softmax-dot over QKV column tiles
 
 struct StageParams {
   CUtensorMap tmap_a;  // activations [m, k] K-major, 128-B swizzle
@@ -55,6 +57,9 @@ struct StageParams {
   float* ws;     // splits > 1: fp32 partial tiles [tiles][splits][BN][128]
   int* cnt;      // splits > 1: per-tile arrival counters (zero on entry and exit)
   int item_begin, item_end;
+  int kind;    // kStageGemm or kStageDot
+  int lda;     // activation leading dimension (elements), used by the dot stage
+  const void* a;  // activations (dot stage reads them with generic loads)
   int in_dep;  // dependency feeding operand A, or -1
   int n_out_deps;
   int out_deps[TS_MAX_DEPS];
@@ -202,6 +207,60 @@ __device__ __forceinline__ void sem_wait(const ChainParams& p, const int* sem, i
   ptx::fence_acq_rel_gpu();
 }
 
+template <typename T>
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const T* h = reinterpret_cast<const T*>(&u);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) f[j] = static_cast<float>(h[j]);
+}
+
+// One row of the fused softmax-dot for head `h`: s = q*v (elementwise over the head's
+// 128 columns), p = softmax(s), out = p*k. Q, K, V are the head's column tiles at
+// offsets h, heads + h and 2*heads + h (x128) of the QKV row.
+template <typename T>
+__device__ __forceinline__ void dot_row(const StageParams& st, int row, int h) {
+  const int heads = st.grid_y;
+  const T* base = reinterpret_cast<const T*>(st.a) + static_cast<size_t>(row) * st.lda;
+  const uint4* q = reinterpret_cast<const uint4*>(base + h * 128);
+  const uint4* k = reinterpret_cast<const uint4*>(base + (heads + h) * 128);
+  const uint4* v = reinterpret_cast<const uint4*>(base + (2 * heads + h) * 128);
+  uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<T*>(st.c) +
+                                        static_cast<size_t>(row) * st.ldc + h * 128);
+  float mx = -INFINITY, sum = 0.f;
+#pragma unroll 4
+  for (int j = 0; j < 16; ++j) {
+    float qf[8], vf[8];
+    unpack8<T>(__ldcg(q + j), qf);
+    unpack8<T>(__ldcg(v + j), vf);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float s = qf[e] * vf[e];
+      if (s > mx) {
+        sum = sum * __expf(mx - s) + 1.f;
+        mx = s;
+      } else {
+        sum += __expf(s - mx);
+      }
+    }
+  }
+  const float inv = 1.f / sum;
+#pragma unroll 4
+  for (int j = 0; j < 16; ++j) {
+    float qf[8], vf[8], kf[8];
+    unpack8<T>(__ldcg(q + j), qf);
+    unpack8<T>(__ldcg(v + j), vf);
+    unpack8<T>(__ldcg(k + j), kf);
+    uint32_t pk[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float o0 = __expf(qf[2 * e] * vf[2 * e] - mx) * inv * kf[2 * e];
+      const float o1 = __expf(qf[2 * e + 1] * vf[2 * e + 1] - mx) * inv * kf[2 * e + 1];
+      pk[e] = pack2<T>(o0, o1);
+    }
+    out[j] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+}
+
 struct Tile {
   int g, s, tb, tx, ty, tz;
 };
@@ -264,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
   }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.n_stages; ++s) {
+      if (p.st[s].kind != kStageGemm) continue;  // pointwise stages have no tensor maps
       ptx::tma_prefetch_desc(&p.st[s].tmap_a);
       ptx::tma_prefetch_desc(&p.st[s].tmap_b);
     }
@@ -342,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         const StageParams& st = p.st[t.s];
         if (leader)
           trace_event(p, ptx::global_timer(), 0, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
+        if (st.kind == kStageDot) continue;  // pointwise stage: the epilogue warps run it
         // activation (dependent) and weight (independent) tile rows of this CTA
         const int act_row = SW ? t.tx * BN : t.tx * C::kTileM + static_cast<int>(rank) * 128;
         const int w_row = SW ? t.ty * 128 : t.ty * BN + static_cast<int>(rank) * C::kBRows;
@@ -438,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         const int g = ring_take(it, false);
         if (g < 0) break;
         const StageParams& sp = p.st[stage_of(p, g)];
+        if (sp.kind == kStageDot) continue;  // no MMA, no accumulator buffer
         const int kblocks = sp.k_blocks / sp.splits;
         const uint32_t acc = local & 1;
         if constexpr (CG == 2) {
@@ -531,6 +593,47 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
       if (g < 0) break;
       const Tile t = decode(p, g);
       const StageParams& st = p.st[t.s];
+      if (st.kind == kStageDot) {
+        // Attention's fused dot: XDot = Dropout(Softmax(XQ . XV)) . XK,
+        // column-tile local as its StridedSync dependency defines it — tile (r, h) reads
+        // only head h's Q, K and V column tiles of row tile r. Dropout p = 0 (inference).
+        // The leader CTA computes the whole tile; its peer (CTA pairs) has nothing to do.
+        if (CG == 2 && !leader) continue;
+        if (threadIdx.x == 128 && st.in_dep >= 0 && !((p.flags >> 12) & 1)) {
+          const DepParams& dp = p.dep[st.in_dep];
+          Wait w = consumer_wait(dp.policy, dp.param, t.tx, t.ty, 0, Grid3{dp.pgx, dp.pgy, dp.pgz},
+                                 dp.pgz);
+          if (w.sem >= 0) {
+            trace_event(p, ptx::global_timer(), 1, t.s, t.tb, 0, st.in_dep, w.sem, w.expected,
+                        t.tx, t.ty, t.tz);
+            sem_wait(p, dp.sem + w.sem, w.expected);
+            trace_event(p, ptx::global_timer(), 2, t.s, t.tb, 0, st.in_dep, w.sem, w.expected,
+                        t.tx, t.ty, t.tz);
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        ptx::fence_acq_rel_gpu();
+#pragma unroll 1
+        for (int rr = ew * 32 + lane; rr < C::kTileM; rr += kEpiThreads) {
+          const int row = t.tx * C::kTileM + rr;
+          if (row < st.m) dot_row<T>(st, row, t.ty);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        if (threadIdx.x == 128) {
+          const uint64_t tnow = ptx::global_timer();
+          __threadfence();
+          ptx::fence_proxy_async_global();
+          for (int i = 0; i < st.n_out_deps; ++i) {
+            const int d = st.out_deps[i];
+            const DepParams& dp = p.dep[d];
+            const int idx = post_target(dp.policy, dp.param, t.tx, t.ty, Grid3{dp.pgx, dp.pgy, dp.pgz});
+            const int old = ptx::atom_add_release_gpu(dp.sem + idx, 1);
+            trace_event(p, tnow, 3, t.s, t.tb, -1, d, idx, old + 1, t.tx, t.ty, t.tz);
+          }
+          trace_event(p, tnow, 4, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
+        }
+        continue;
+      }
       const uint32_t acc = local & 1;
       if constexpr (CG == 2) {
         ptx::mbar_wait(&tmem_full[acc], (local >> 1) & 1);  // arrived by the MMA commit

@@ -60,6 +60,7 @@ class CuStage:
     splits: int = 1
     ws: torch.Tensor | None = None
     cnt: torch.Tensor | None = None
+    kind: str = "gemm"  # "gemm" or "dot" (attention's fused softmax-dot)
 
     @property
     def m(self) -> int:
@@ -67,7 +68,8 @@ class CuStage:
 
     @property
     def n(self) -> int:
-        return self.b.shape[0]
+        """Output columns (accumulator columns for SwiGLU)."""
+        return self.c.shape[1] if self.kind == "dot" else self.b.shape[0]
 
     @property
     def k(self) -> int:
@@ -76,7 +78,7 @@ class CuStage:
     @property
     def out_tile_cols(self) -> int:
         """Output columns one tile writes (a consumer k-step in reference units)."""
-        if self.cs.swap_ab:
+        if self.cs.swap_ab or self.kind == "dot":
             return 128
         return self.cs.tile_n // 2 if self.epilogue == "swiglu" else self.cs.tile_n
 
@@ -84,11 +86,11 @@ class CuStage:
     def grid(self) -> Dim3:
         """Tile grid as the reference's Stage.grid sees it: (activation-row tiles,
         output-column tiles, split-K slices)."""
-        cols = 128 if self.cs.swap_ab else self.cs.tile_n
+        cols = 128 if (self.cs.swap_ab or self.kind == "dot") else self.cs.tile_n
         return Dim3(-(-self.m // self.cs.tile_m), max(1, self.n // cols), self.splits)
 
     def flops(self) -> int:
-        return 2 * self.m * self.n * self.k
+        return 0 if self.kind == "dot" else 2 * self.m * self.n * self.k
 
 
 @dataclass
@@ -179,6 +181,26 @@ class CuSync:
         self._desc = None
         return st
 
+    def stage_dot(self, qkv: torch.Tensor, out: torch.Tensor, order: TileOrder = RowMajor(),
+                  id: str | None = None) -> CuStage:
+        """Attention's fused dot kernel: ``out`` [m, n] =
+        Dropout(Softmax(XQ . XV)) . XK per 128-column head, with ``qkv`` [m, 3n] holding
+        [Q heads | K heads | V heads]. Column-tile local, as its StridedSync dependency
+        defines it; dropout p = 0 (inference)."""
+        if len(self.stages) >= _lib.TS_MAX_STAGES:
+            raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
+        for t, name in ((qkv, "qkv"), (out, "out")):
+            if t.dim() != 2 or t.stride(1) != 1 or t.dtype not in _DT or not t.is_cuda:
+                raise ValueError(f"{name} must be a row-major fp16/bf16 CUDA matrix")
+        if qkv.shape[0] != out.shape[0] or qkv.shape[1] != 3 * out.shape[1]:
+            raise ValueError(f"qkv must be [m, 3n] for out [m, n], got {tuple(qkv.shape)}")
+        st = CuStage(self, len(self.stages), id or f"dot{len(self.stages) + 1}", qkv, qkv, out,
+                     "none", order, kind="dot")
+        self.stages.append(st)
+        self.device = qkv.device
+        self._desc = None
+        return st
+
     def dependency(self, policy: SyncPolicy, producer: CuStage, consumer: CuStage,
                    operand: str = "a") -> CuDep:
         """cs.dependency<Policy>(prod, cons, operand) — allocates the semaphore array."""
@@ -198,14 +220,17 @@ class CuSync:
         stages = []
         for st in self.stages:
             d = in_dep.get(st.index)
-            if d is None:
+            if st.kind == "dot":
+                k_steps = 1  # attention_scenario's dot stage (workloads.py:124-153)
+            elif d is None:
                 k_steps = max(1, st.k // st.out_tile_cols)
             else:
                 k_steps = st.k // d.producer.out_tile_cols
                 if isinstance(d.policy, Conv2DTileSync):
                     k_steps *= d.policy.kk
+            operands = ("qkv",) if st.kind == "dot" else ("a", "b")
             stages.append(Stage(id=st.id, grid=st.grid, occupancy=1, k_steps=k_steps,
-                                order=st.order))
+                                order=st.order, operands=operands))
         deps = tuple(Dependency(d.producer.id, d.consumer.id, d.operand, d.policy)
                      for d in self.deps)
         mode = Mode.FINE if self.mode == "fused" else Mode.STREAM
@@ -226,14 +251,16 @@ class CuSync:
             sd.epilogue = _EPI[st.epilogue]
             sd.order, sd.order_stride = order_code(st.order)
             sd.splits = st.splits
+            sd.kind = _lib.TS_STAGE_ATTN_DOT if st.kind == "dot" else _lib.TS_STAGE_GEMM
             sd.workspace = st.ws.data_ptr() if st.ws is not None else None
             sd.counters = st.cnt.data_ptr() if st.cnt is not None else None
         d.n_deps = len(self.deps)
         for i, dep in enumerate(self.deps):
             dd = d.deps[i]
             dd.producer, dd.consumer = dep.producer.index, dep.consumer.index
-            if dep.operand != "a":
-                raise ConfigError("GeMM stages consume their producer through operand 'a'")
+            if dep.operand != ("qkv" if dep.consumer.kind == "dot" else "a"):
+                raise ConfigError("GeMM stages consume their producer through operand 'a', "
+                                  "the dot stage through 'qkv'")
             dd.operand = 0
             dd.policy, dd.param = policy_code(dep.policy)
             dd.sem = dep.sem.data_ptr()
