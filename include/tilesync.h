@@ -138,7 +138,8 @@ typedef enum {
   TS_STAGE_ATTN_DOT = 1 /* attention's fused dot: a = XQKV [m, 3n] with
                            [Q heads | K heads | V heads] 128-column head tiles, c = XDot
                            [m, n]; XDot = Softmax(Q*V)*K per head and row (column-tile
-                           local, dropout p = 0); b unused. Tile = rows x one head.     */
+                           local, dropout p = 0); b unused. Tile = rows x tile_n columns
+                           (tile_n / 128 heads).                                         */
 } ts_stage_kind;
 
 typedef struct {

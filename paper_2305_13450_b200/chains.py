@@ -99,23 +99,24 @@ class AttentionChain:
     def __init__(self, x: torch.Tensor, w_qkv: torch.Tensor, w2: torch.Tensor,
                  second_policy: SyncPolicy | None = None, mode: str = "fused",
                  cta_group: int = 2, keep_sems: bool = False, num_ctas: int = 0,
-                 extra_flags: int = 0):
+                 extra_flags: int = 0, tile_n: int = 256):
         from .policies import StridedRowMajor, StridedSync, TileSync
         m = x.shape[0]
         n3 = w_qkv.shape[0]
-        if n3 % (3 * 128):
-            raise ValueError("Wqkv rows must be 3 x heads x 128")
-        heads = n3 // (3 * 128)
-        self.heads = heads
+        if n3 % (3 * tile_n):
+            raise ValueError(f"Wqkv rows must be 3 x (a multiple of tile_n={tile_n})")
+        self.heads = n3 // (3 * 128)
+        # column tiles per Q/K/V third = the StridedSync stride H / (8 Ty)
+        stride = n3 // (3 * tile_n)
         self.qkv = torch.empty(m, n3, dtype=x.dtype, device=x.device)
         self.dot = torch.empty(m, n3 // 3, dtype=x.dtype, device=x.device)
         self.y = torch.empty(m, w2.shape[0], dtype=x.dtype, device=x.device)
-        self.cs = CuSync(tile_n=128, mode=mode, cta_group=cta_group, keep_sems=keep_sems,
+        self.cs = CuSync(tile_n=tile_n, mode=mode, cta_group=cta_group, keep_sems=keep_sems,
                          num_ctas=num_ctas, extra_flags=extra_flags)
-        self.s_qkv = self.cs.stage(x, w_qkv, self.qkv, order=StridedRowMajor(heads), id="qkv")
+        self.s_qkv = self.cs.stage(x, w_qkv, self.qkv, order=StridedRowMajor(stride), id="qkv")
         self.s_dot = self.cs.stage_dot(self.qkv, self.dot, id="dot")
         self.s_out = self.cs.stage(self.dot, w2, self.y, id="out")
-        self.cs.dependency(StridedSync(heads), self.s_qkv, self.s_dot, operand="qkv")
+        self.cs.dependency(StridedSync(stride), self.s_qkv, self.s_dot, operand="qkv")
         self.cs.dependency(second_policy or TileSync(), self.s_dot, self.s_out, operand="a")
 
     def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:

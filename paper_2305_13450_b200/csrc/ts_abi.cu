@@ -200,8 +200,8 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     if (st.dtype != dtype) return fail(TS_ERR_CONFIG, "stage %d: all stages must share a dtype", s);
     if (st.kind == TS_STAGE_ATTN_DOT) {
       if (swap) return fail(TS_ERR_CONFIG, "stage %d: the attention dot stage needs normal tiles", s);
-      if (st.m < 1 || st.n < 128 || st.n % 128)
-        return fail(TS_ERR_CONFIG, "stage %d: dot width %d must be a positive multiple of 128", s, st.n);
+      if (st.m < 1 || st.n < bn || st.n % bn)
+        return fail(TS_ERR_CONFIG, "stage %d: dot width %d must be a positive multiple of tile_n %d", s, st.n, bn);
       if (st.lda < 3 * st.n || st.lda % 8 || st.ldc < st.n || st.ldc % 8)
         return fail(TS_ERR_VALUE, "stage %d: dot needs lda >= 3n and ldc >= n (multiples of 8)", s);
       if (!st.a || !st.c) return fail(TS_ERR_VALUE, "stage %d: null operand pointer", s);
@@ -217,7 +217,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       sp.n = st.n;
       sp.ldc = st.ldc;
       sp.grid_x = (st.m + tile_m - 1) / tile_m;
-      sp.grid_y = st.n / 128;
+      sp.grid_y = st.n / bn;  // one tile = tile_n columns = tile_n / 128 heads
       sp.splits = 1;
       sp.order = st.order;
       sp.order_stride = st.order == TS_ORDER_ROW_MAJOR ? 1 : (st.order_stride < 1 ? 1 : st.order_stride);
@@ -227,6 +227,8 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       sp.item_end = items;
       sp.in_dep = -1;
       sp.n_out_deps = 0;
+      sp.dot_dep = -1;
+      sp.last_arriver = 0;
       continue;
     }
     if (st.kind != TS_STAGE_GEMM) return fail(TS_ERR_TYPE, "stage %d: unknown stage kind %d", s, st.kind);
@@ -283,6 +285,8 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.item_end = items;
     sp.in_dep = -1;
     sp.n_out_deps = 0;
+    sp.dot_dep = -1;
+    sp.last_arriver = 0;
     if (with_tmaps) {
       // activations: box rows = 128 per CTA (normal) or tile_n (swapped);
       // weights: box rows = tile_n / cta_group (normal) or 128 (swapped)
@@ -314,7 +318,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
                   cs.grid_x, ps.grid_x);
     if (cs.in_dep >= 0)
       return fail(TS_ERR_CONFIG, "dependency %d: stage %d already has an operand-A dependency", i, dd.consumer);
-    const int cols = ps.kind == ts::kStageDot ? 128 : out_tile_cols(d->stages[dd.producer], bn, swap);
+    const int cols = ps.kind == ts::kStageDot ? bn : out_tile_cols(d->stages[dd.producer], bn, swap);
     int kb_per_kstep = cols / ts::kBK;
     int k_steps = 0;
     if (cs.kind == ts::kStageDot) {
@@ -349,9 +353,36 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     dp.pgz = pg.z;
     dp.kb_per_kstep = kb_per_kstep;
     dp.sem_n = ts::sem_count(dd.policy, dd.param, pg);
+    dp.consumer = dd.consumer;
     cs.in_dep = i;
     ts::StageParams& pw = p->st[dd.producer];
     pw.out_deps[pw.n_out_deps++] = i;
+  }
+  // Fused launches run a GeMM-fed dot stage on the last-arriving producer CTA (its
+  // tiles leave the claim list); diagnostic flag bit 16 keeps them as claimed items.
+  if (d->mode == TS_MODE_FUSED && !((d->flags >> 16) & 1)) {
+    bool changed = false;
+    for (int i = 0; i < d->n_deps; ++i) {
+      ts::StageParams& ps = p->st[d->deps[i].producer];
+      ts::StageParams& cs = p->st[d->deps[i].consumer];
+      if (cs.kind == ts::kStageDot && ps.kind == ts::kStageGemm && cs.grid_y <= 32 &&
+          ps.dot_dep < 0 && cs.in_dep == i) {
+        cs.last_arriver = 1;
+        ps.dot_dep = i;
+        changed = true;
+      }
+    }
+    if (changed) {
+      int next = 0;
+      for (int s = 0; s < p->n_stages; ++s) {
+        ts::StageParams& sp = p->st[s];
+        const int n = sp.last_arriver ? 0 : sp.item_end - sp.item_begin;
+        sp.item_begin = next;
+        next += n;
+        sp.item_end = next;
+      }
+      p->total_items = next;
+    }
   }
   return TS_OK;
 }
@@ -487,6 +518,7 @@ int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
   for (int i = 0; i < q.n_stages; ++i) {
     q.st[i].in_dep = -1;
     q.st[i].n_out_deps = 0;
+    q.st[i].dot_dep = -1;
   }
   for (int i = 0; i < q.n_stages; ++i) {
     q.item_lo = q.st[i].item_begin;

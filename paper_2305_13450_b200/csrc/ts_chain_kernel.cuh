@@ -63,6 +63,11 @@ struct StageParams {
   int in_dep;  // dependency feeding operand A, or -1
   int n_out_deps;
   int out_deps[TS_MAX_DEPS];
+  // Last-arriver dot (fused mode): the dot stage's tiles are not claimed from the work
+  // counter; the producer CTA whose post completes a dot tile's wait runs that tile
+  // right away. `dot_dep` is this (producer) stage's dependency into such a dot stage.
+  int dot_dep;       // producer side: dependency index, or -1
+  int last_arriver;  // dot side: 1 when its tiles run on the last-arriving producer
 };
 
 struct DepParams {
@@ -71,6 +76,7 @@ struct DepParams {
   int pgx, pgy, pgz;    // producer grid (reference Stage.grid)
   int kb_per_kstep;     // consumer K-blocks per reference k-step
   int sem_n;
+  int consumer;         // consumer stage index
 };
 
 struct ChainParams {
@@ -108,7 +114,8 @@ struct Cfg {
   static constexpr int kBarOffset = kStages * kStageBytes;
   // full, empty per stage; tmem full/empty x2; tile ring full/empty; peer_done x2
   static constexpr int kNumBars = 2 * kStages + 4 + 2 * kTileRing + 2;
-  static constexpr int kSmemBytes = 1024 + kBarOffset + kNumBars * 8 + 64;
+  // + tile ring ids, TMEM slot, flags and the last-arriver dot list (64 ints)
+  static constexpr int kSmemBytes = 1024 + kBarOffset + kNumBars * 8 + 64 + 272;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
   static_assert(kBRows % 8 == 0 && kBRows <= 256, "B box rows");
 };
@@ -219,7 +226,7 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
 // offsets h, heads + h and 2*heads + h (x128) of the QKV row.
 template <typename T>
 __device__ __forceinline__ void dot_row(const StageParams& st, int row, int h) {
-  const int heads = st.grid_y;
+  const int heads = st.n / 128;
   const T* base = reinterpret_cast<const T*>(st.a) + static_cast<size_t>(row) * st.lda;
   const uint4* q = reinterpret_cast<const uint4*>(base + h * 128);
   const uint4* k = reinterpret_cast<const uint4*>(base + (heads + h) * 128);
@@ -298,6 +305,8 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ti_item + kTileRing);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   int* split_flag = last_flag + 1;
+  int* dot_count = split_flag + 1;  // last-arriver dot tiles released by a post
+  int* dot_list = dot_count + 1;    // [0, 32): dot tile columns, [32, 64): their tb
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -319,6 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
       // leader MMA warp + every epilogue warp of the pair + the peer's producer lane
       ptx::mbar_init(&ti_empty[i], 1 + CG * kEpiThreads / 32 + (CG - 1));
     }
+    *dot_count = 0;
     ptx::fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -587,6 +597,36 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         }
       }
     }
+    // Compute dot tile (tx, ty) of stage ds with the 128 epilogue threads (its wait is
+    // already satisfied), then post to its consumers (thread 128).
+    auto run_dot = [&](int ds, int tx, int ty, int tb) {
+      const StageParams& sd = p.st[ds];
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+      ptx::fence_acq_rel_gpu();
+#pragma unroll 1
+      for (int rr = ew * 32 + lane; rr < C::kTileM; rr += kEpiThreads) {
+        const int row = tx * C::kTileM + rr;
+        if (row < sd.m) {
+          // a dot tile covers BN / 128 heads (the paper's stride H / (8 Ty))
+#pragma unroll 1
+          for (int hh = 0; hh < BN / 128; ++hh) dot_row<T>(sd, row, ty * (BN / 128) + hh);
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+      if (threadIdx.x == 128) {
+        const uint64_t tnow = ptx::global_timer();
+        __threadfence();
+        ptx::fence_proxy_async_global();
+        for (int i = 0; i < sd.n_out_deps; ++i) {
+          const int d = sd.out_deps[i];
+          const DepParams& dp = p.dep[d];
+          const int idx = post_target(dp.policy, dp.param, tx, ty, Grid3{dp.pgx, dp.pgy, dp.pgz});
+          const int old = ptx::atom_add_release_gpu(dp.sem + idx, 1);
+          trace_event(p, tnow, 3, ds, tb, -1, d, idx, old + 1, tx, ty);
+        }
+        trace_event(p, tnow, 4, ds, tb, -1, -1, -1, -1, tx, ty);
+      }
+    };
 #pragma unroll 1
     for (int it = 0;; ++it) {
       const int g = ring_take(it, CG == 2 && !leader);
@@ -611,27 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
                         t.tx, t.ty, t.tz);
           }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-        ptx::fence_acq_rel_gpu();
-#pragma unroll 1
-        for (int rr = ew * 32 + lane; rr < C::kTileM; rr += kEpiThreads) {
-          const int row = t.tx * C::kTileM + rr;
-          if (row < st.m) dot_row<T>(st, row, t.ty);
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-        if (threadIdx.x == 128) {
-          const uint64_t tnow = ptx::global_timer();
-          __threadfence();
-          ptx::fence_proxy_async_global();
-          for (int i = 0; i < st.n_out_deps; ++i) {
-            const int d = st.out_deps[i];
-            const DepParams& dp = p.dep[d];
-            const int idx = post_target(dp.policy, dp.param, t.tx, t.ty, Grid3{dp.pgx, dp.pgy, dp.pgz});
-            const int old = ptx::atom_add_release_gpu(dp.sem + idx, 1);
-            trace_event(p, tnow, 3, t.s, t.tb, -1, d, idx, old + 1, t.tx, t.ty, t.tz);
-          }
-          trace_event(p, tnow, 4, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
-        }
+        run_dot(t.s, t.tx, t.ty, t.tb);
         continue;
       }
       const uint32_t acc = local & 1;
@@ -818,10 +838,40 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
                                           Grid3{dp.pgx, dp.pgy, dp.pgz});
               const int old = ptx::atom_add_release_gpu(dp.sem + idx, 1);
               trace_event(p, tnow, 3, t.s, t.tb, -1, d, idx, old + 1, t.tx, t.ty, t.tz);
+              if (d == st.dot_dep) {
+                // Which dot tiles of this row did this post complete? (the wait of tile
+                // (x, c) at k-step 0 is on semaphore idx and now reached its threshold)
+                const StageParams& sd = p.st[dp.consumer];
+                int n = 0;
+                for (int c = 0; c < sd.grid_y; ++c) {
+                  Wait w = consumer_wait(dp.policy, dp.param, t.tx, c, 0,
+                                         Grid3{dp.pgx, dp.pgy, dp.pgz}, dp.pgz);
+                  if (w.sem == idx && w.expected == old + 1) {
+                    const int tb = atomicAdd(&p.scratch[4], 1);
+                    dot_list[n] = c;
+                    dot_list[32 + n] = tb;
+                    ++n;
+                    // the dot tile is scheduled the moment its wait is satisfied
+                    trace_event(p, tnow, 0, dp.consumer, tb, -1, -1, -1, -1, t.tx, c);
+                    trace_event(p, tnow, 1, dp.consumer, tb, 0, d, idx, w.expected, t.tx, c);
+                    trace_event(p, tnow, 2, dp.consumer, tb, 0, d, idx, w.expected, t.tx, c);
+                  }
+                }
+                *dot_count = n;
+              }
             }
           }
           trace_event(p, tnow, 4, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
         }
+      }
+      if (st.dot_dep >= 0 && leader) {
+        // last-arriver dot tiles released by this tile's posts
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        const int n = *dot_count;
+        const int ds = p.dep[st.dot_dep].consumer;
+        for (int i = 0; i < n; ++i) run_dot(ds, t.tx, dot_list[i], dot_list[32 + i]);
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        if (threadIdx.x == 128) *dot_count = 0;
       }
       ++local;
     }
@@ -853,6 +903,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
     if (threadIdx.x == 0) {
       p.scratch[0] = 0;
       p.scratch[1] = 0;
+      p.scratch[4] = 0;  // last-arriver dot claim counter
     }
     __threadfence();
   }

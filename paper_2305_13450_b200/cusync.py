@@ -78,7 +78,7 @@ class CuStage:
     @property
     def out_tile_cols(self) -> int:
         """Output columns one tile writes (a consumer k-step in reference units)."""
-        if self.cs.swap_ab or self.kind == "dot":
+        if self.cs.swap_ab:
             return 128
         return self.cs.tile_n // 2 if self.epilogue == "swiglu" else self.cs.tile_n
 
@@ -86,7 +86,7 @@ class CuStage:
     def grid(self) -> Dim3:
         """Tile grid as the reference's Stage.grid sees it: (activation-row tiles,
         output-column tiles, split-K slices)."""
-        cols = 128 if (self.cs.swap_ab or self.kind == "dot") else self.cs.tile_n
+        cols = 128 if self.cs.swap_ab else self.cs.tile_n
         return Dim3(-(-self.m // self.cs.tile_m), max(1, self.n // cols), self.splits)
 
     def flops(self) -> int:

@@ -261,10 +261,13 @@ def test_split_trace_counts_follow_reference_z(pol, z1, z2):
         cons_slices * sum(n for (_, n) in dag.values())
 
 
-@pytest.mark.parametrize("m,heads,cg,mode", [(256, 2, 2, "fused"), (300, 3, 1, "fused"),
-                                            (520, 2, 2, "stream"), (128, 4, 1, "fused")])
+@pytest.mark.parametrize("m,heads,cg,mode,tn", [(256, 2, 2, "fused", 256),
+                                               (300, 3, 1, "fused", 128),
+                                               (520, 2, 2, "stream", 256),
+                                               (128, 4, 1, "fused", 256),
+                                               (200, 4, 2, "fused", 128)])
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
-def test_attention_chain(m, heads, cg, mode, dtype):
+def test_attention_chain(m, heads, cg, mode, tn, dtype):
     """QKV (StridedRowMajor) -> fused dot (StridedSync) -> out GeMM (TileSync)."""
     g = torch.Generator().manual_seed(11)
     h = 512
@@ -272,7 +275,7 @@ def test_attention_chain(m, heads, cg, mode, dtype):
     wqkv = (torch.randn(3 * heads * 128, h, generator=g) / h ** 0.5).to(dtype)
     w2 = (torch.randn(h, heads * 128, generator=g) / (heads * 128) ** 0.5).to(dtype)
     ch = ts.AttentionChain(x.cuda(), wqkv.cuda(), w2.cuda(), mode=mode, cta_group=cg,
-                           keep_sems=(mode == "fused"))
+                           keep_sems=(mode == "fused"), tile_n=tn)
     ch.cs.enable_trace()
     ch()
     torch.cuda.synchronize()
@@ -298,6 +301,9 @@ def test_attention_chain(m, heads, cg, mode, dtype):
     assert O.validate_trace(evs, stages, deps, fine=(mode == "fused")) == []
     for st in sc.stages:  # tiles drawn in order_tile order (StridedRowMajor for qkv)
         sched = [e for e in evs if e["stage"] == st.id and e["kind"] == "scheduled"]
+        assert sorted(e["tb"] for e in sched) == list(range(st.grid.total()))
+        if st.id == "dot" and mode == "fused":
+            continue  # last-arriver dot tiles are claimed in completion order
         for e in sched:
             t = ts.order_tile(st.order, st.grid, e["tb"])
             assert tuple(e["tile"]) == (t.x, t.y, 0)
