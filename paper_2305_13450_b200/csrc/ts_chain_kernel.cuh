@@ -842,6 +842,8 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
                 // Which dot tiles of this row did this post complete? (the wait of tile
                 // (x, c) at k-step 0 is on semaphore idx and now reached its threshold)
                 const StageParams& sd = p.st[dp.consumer];
+                // time read after the atomic: later than every post it counted
+                const uint64_t tfire = ptx::global_timer();
                 int n = 0;
                 for (int c = 0; c < sd.grid_y; ++c) {
                   Wait w = consumer_wait(dp.policy, dp.param, t.tx, c, 0,
@@ -852,9 +854,9 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
                     dot_list[32 + n] = tb;
                     ++n;
                     // the dot tile is scheduled the moment its wait is satisfied
-                    trace_event(p, tnow, 0, dp.consumer, tb, -1, -1, -1, -1, t.tx, c);
-                    trace_event(p, tnow, 1, dp.consumer, tb, 0, d, idx, w.expected, t.tx, c);
-                    trace_event(p, tnow, 2, dp.consumer, tb, 0, d, idx, w.expected, t.tx, c);
+                    trace_event(p, tfire, 0, dp.consumer, tb, -1, -1, -1, -1, t.tx, c);
+                    trace_event(p, tfire, 1, dp.consumer, tb, 0, d, idx, w.expected, t.tx, c);
+                    trace_event(p, tfire, 2, dp.consumer, tb, 0, d, idx, w.expected, t.tx, c);
                   }
                 }
                 *dot_count = n;
