@@ -231,10 +231,21 @@ def main():
     chain = ts.MlpChain(x, w1, w2, **best)
     stream_chain = ts.MlpChain(x, w1, w2, **base)
 
+    kernel_events = []  # (start, end) CUDA events around each chain launch, timed region
+
     def step():
-        y = chain()
+        if record_kernel[0]:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            y = chain()
+            e1.record()
+            kernel_events.append((e0, e1))
+        else:
+            y = chain()
         if use_dist:
             dist.all_reduce(y)
+
+    record_kernel = [False]
 
     def step_stream():
         y = stream_chain()
@@ -251,12 +262,15 @@ def main():
         step()
     torch.cuda.synchronize()
     with sampler:
+        record_kernel[0] = True
         us = time_steps(step, args.steps, 0, torch, dist if use_dist else None)
+        record_kernel[0] = False
     us_stream = time_steps(step_stream, args.steps, args.warmup, torch, dist if use_dist else None)
     us_cublas = time_steps(step_cublas, args.steps, args.warmup, torch, dist if use_dist else None)
 
-    # kernel-only duration of the chain launch (roofline numerator): single-rank chain
-    us_kernel = time_steps(chain, args.steps, args.warmup, torch, None)
+    # kernel-only duration of the chain launch (roofline denominator): the average of the
+    # per-launch CUDA-event durations recorded inside the timed region, on the launch stream
+    us_kernel = statistics.mean(a.elapsed_time(b) for a, b in kernel_events) * 1e3
     assert not chain.cs.watchdog_fired(), "semaphore watchdog fired"
 
     # end to end through the public API with host buffers: pinned X -> device, chain,
@@ -275,7 +289,8 @@ def main():
 
     sweep = None
     if rank == 0 and world == 1 and not args.no_sweep:
-        sweep = planner.sweep_mlp(batches=(1, 64, 256, 512, 1024, 2048), device=dev)
+        sweep = {"gpt3_mlp": planner.sweep_mlp(batches=(1, 64, 256, 512, 1024, 2048), device=dev),
+                 "gpt3_attention": planner.sweep_attention(device=dev)}
 
     if rank != 0:
         if use_dist:

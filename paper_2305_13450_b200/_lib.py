@@ -13,7 +13,8 @@ from pathlib import Path
 
 from .errors import ConfigError
 
-LIB_PATH = Path(__file__).resolve().parent / "libtilesync_b200.so"
+LIB_PATH = Path(os.environ.get("TS_LIB_PATH",
+                               Path(__file__).resolve().parent / "libtilesync_b200.so"))
 
 TS_OK, TS_ERR_CONFIG, TS_ERR_VALUE, TS_ERR_TYPE, TS_ERR_CUDA, TS_ERR_DEADLOCK = range(6)
 

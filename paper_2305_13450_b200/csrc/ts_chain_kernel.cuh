@@ -545,19 +545,18 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
           if (lane == 0) {
             const uint32_t a_addr = ptx::smem_u32(sA + rs * C::kABytes);
             const uint32_t b_addr = ptx::smem_u32(sB + rs * C::kBBytes);
+            if constexpr (C::kAcc > 1) {
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) {
-              const uint64_t ad = ptx::smem_desc_k_sw128(a_addr + k * 32);
-              const uint64_t bd = ptx::smem_desc_k_sw128(b_addr + k * 32);
-              if constexpr (CG == 2) {
-                ptx::umma_f16_pair(d_tmem, ad, bd, kIdesc, (kb | k) != 0);
-              } else if constexpr (C::kAcc > 1) {
+              for (int k = 0; k < kBK / 16; ++k) {
+                const uint64_t ad = ptx::smem_desc_k_sw128(a_addr + k * 32);
+                const uint64_t bd = ptx::smem_desc_k_sw128(b_addr + k * 32);
                 const int step = kb * (kBK / 16) + k;  // rotate independent accumulators
-                ptx::umma_f16(d_tmem + (step % C::kAcc) * BN, ad, bd, kIdesc,
-                              step >= C::kAcc);
-              } else {
-                ptx::umma_f16(d_tmem, ad, bd, kIdesc, (kb | k) != 0);
+                ptx::umma_f16(d_tmem + (step % C::kAcc) * BN, ad, bd, kIdesc, step >= C::kAcc);
               }
+            } else {
+              // the K-block's four MMAs back to back in one issue sequence
+              ptx::umma_f16_kblock<CG>(d_tmem, ptx::smem_desc_k_sw128(a_addr),
+                                       ptx::smem_desc_k_sw128(b_addr), kIdesc, kb != 0);
             }
             if constexpr (CG == 2) {
               ptx::umma_commit_pair(&empty[rs]);

@@ -105,6 +105,41 @@ def sweep_mlp(batches=(1, 64, 256, 512, 1024, 2048), hidden=12288, ffn=6144, dev
     return rows
 
 
+def _torch_attention(x, wqkv, w2, heads):
+    m = x.shape[0]
+    qkv = x @ wqkv.t()
+    q, k, v = qkv.view(m, 3, heads, 128).unbind(1)
+    dot = (torch.softmax((q * v).float(), dim=-1) * k.float()).to(x.dtype).reshape(m, -1)
+    return dot @ w2.t()
+
+
+def sweep_attention(seqs=(512, 1024, 2048), hidden=12288, heads=12, device=None):
+    """GPT-3 attention block (TP=8 shard): QKV -> fused dot -> out, fused vs stream vs a
+    torch/cuBLAS implementation of the same math."""
+    from .chains import AttentionChain
+    torch.manual_seed(8)
+    wqkv = (torch.randn(3 * heads * 128, hidden, device=device) / hidden ** 0.5).half()
+    w2 = (torch.randn(hidden, heads * 128, device=device) / (heads * 128) ** 0.5).half()
+    rows = []
+    for s in seqs:
+        x = torch.randn(s, hidden, device=device).half()
+        best = {}
+        for mode in ("fused", "stream"):
+            for cg in (1, 2):
+                for pol in ([RowSync(), TileSync()] if mode == "fused" else [TileSync()]):
+                    ch = AttentionChain(x, wqkv, w2, second_policy=pol, mode=mode, cta_group=cg)
+                    us = _time(ch, iters=20)
+                    if us < best.get(mode, (float("inf"),))[0]:
+                        best[mode] = (us, {"cta_group": cg, "policy": type(pol).__name__})
+        cu = _time(lambda: _torch_attention(x, wqkv, w2, heads), iters=20)
+        flops = 2 * s * hidden * 3 * heads * 128 + 2 * s * heads * 128 * hidden
+        rows.append({"seq": s, "fused_us": best["fused"][0], "stream_us": best["stream"][0],
+                     "torch_us": cu, "speedup_vs_stream": best["stream"][0] / best["fused"][0],
+                     "fused_tflops": flops / best["fused"][0] / 1e6,
+                     "fused": best["fused"][1], "stream": best["stream"][1]})
+    return rows
+
+
 def wave_table(m: int, n1: int, n2: int, tile_m: int, tile_n: int, sms: int = 148):
     """Stream vs fused whole-wave counts for the two GeMMs."""
     units = sms // (tile_m // 128)

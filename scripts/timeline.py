@@ -48,17 +48,24 @@ def summarize(cs, label):
         print(f"  {st.id}: tiles {len(d)} dur mean {sum(d) / len(d) / 1e3:.1f} us "
               f"min {min(d) / 1e3:.1f} max {max(d) / 1e3:.1f}; wait mean {sum(w) / len(w) / 1e3:.2f} us "
               f"max {max(w) / 1e3:.1f}; span {s0 / 1e3:.1f}..{f1 / 1e3:.1f} us")
-    mb = {(r.stage, r.tb): r.t_ns for r in recs if r.kind == 5}
+    mbr = {(r.stage, r.tb): r for r in recs if r.kind == 5}
+    mb = {k: r.t_ns for k, r in mbr.items()}
     me = {(r.stage, r.tb): r for r in recs if r.kind == 6}
     t0 = min(r.t_ns for r in recs)
     for s_i, st in enumerate(cs.stages):
         keys = [k for k in me if k[0] == s_i and k in mb and k in start]
         if keys:
             mma = [me[k].t_ns - mb[k] for k in keys]
+            cyc = [(me[k].clk - mbr[k].clk) % (1 << 32) for k in keys if me[k].smid == mbr[k].smid]
             starve = [me[k].value for k in keys]
             lead = [mb[k] - start[k].t_ns for k in keys]
-            print(f"  {st.id}: MMA span mean {sum(mma) / len(mma) / 1e3:.1f} us, operand-starved "
-                  f"{sum(starve) / len(starve) / 1e3:.1f} us, claim->first MMA "
+            # ideal tensor cycles of one tile: 4096 MAC/clk per SM (8192 per CTA pair)
+            macs = cs.tile_m * (128 if cs.swap_ab else cs.tile_n) * st.k // max(1, st.splits)
+            ideal = macs / (4096 * (2 if cs.cta_group == 2 else 1))
+            eff = (f", {sum(cyc) / len(cyc):.0f} cycles = {ideal / (sum(cyc) / len(cyc)) * 100:.0f}%"
+                   f" of the MMA floor") if cyc and st.kind == "gemm" else ""
+            print(f"  {st.id}: MMA span mean {sum(mma) / len(mma) / 1e3:.1f} us{eff}, "
+                  f"operand-starved {sum(starve) / len(starve) / 1e3:.1f} us, claim->first MMA "
                   f"{sum(lead) / len(lead) / 1e3:.1f} us")
     # MMA idle per CTA(-pair leader): before its first tile, between tiles, after its last
     per_sm = defaultdict(list)
