@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 1
+#define TS_ABI_VERSION 2
 
 /* ---- status codes ---------------------------------------------------------------- */
 typedef enum {
@@ -131,6 +131,11 @@ typedef struct {
   float* workspace;  /* splits > 1: device fp32[tiles * splits * tile_n * 128]         */
   int* counters;     /* splits > 1: device int32[tiles], zero on entry (kept zero)     */
   int kind;          /* ts_stage_kind */
+  int tile_n;        /* this stage's tile width: 0 = the chain's tile_n; 512 = a
+                        double-width CTA-pair tile (256 x 512 outputs: one A box feeds
+                        two N = 256 MMAs, 25 % fewer operand bytes per MAC), allowed
+                        for GeMM stages of cta_group 2, tile_n 256 chains that do not
+                        feed a dot stage */
 } ts_stage_desc;
 
 typedef enum {
@@ -176,7 +181,8 @@ typedef struct {
   uint64_t t_ns;     /* %globaltimer */
   int32_t kind;      /* 0 scheduled, 1 wait_begin, 2 wait_end, 3 post, 4 finished;
                         extensions: 5 mma_begin, 6 mma_end (value = ns the tile's MMAs
-                        waited for operands after the first stage) */
+                        waited for operands after the first stage), 7 epilogue_begin
+                        (accumulator ready), 8 epilogue_end (thread 0's stores issued) */
   int32_t stage;     /* stage index */
   int32_t tb;        /* claim index within the stage (reference `tb`) */
   int32_t k;         /* reference k-step, -1 = none */

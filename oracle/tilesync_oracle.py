@@ -244,17 +244,12 @@ def validate_trace(events, stages, deps, fine=True):
 
 # ---- numerics -----------------------------------------------------------
 
-def _erf(x):
-    try:
-        from scipy.special import erf
-        return erf(x)
-    except ImportError:  # pragma: no cover - scipy is in the image
-        return np.vectorize(math.erf)(x)
-
-
 def gelu(x):
-    """Exact (erf) GeLU, the form the device epilogue implements."""
-    return 0.5 * x * (1.0 + _erf(x / math.sqrt(2.0)))
+    """GeLU in GPT-3's tanh form ("gelu_new", the MLP activation of GPT-2/3):
+    0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))) — the form the device epilogue
+    implements (with the hardware tanh approximation; its error is far inside the
+    fp16/bf16 tolerance of the parity tests)."""
+    return 0.5 * x * (1.0 + np.tanh(math.sqrt(2.0 / math.pi) * (x + 0.044715 * x * x * x)))
 
 
 def silu(x):

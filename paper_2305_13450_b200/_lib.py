@@ -47,7 +47,7 @@ class StageDesc(ctypes.Structure):
         ("dtype", ctypes.c_int), ("epilogue", ctypes.c_int),
         ("order", ctypes.c_int), ("order_stride", ctypes.c_int),
         ("splits", ctypes.c_int), ("workspace", ctypes.c_void_p),
-        ("counters", ctypes.c_void_p), ("kind", ctypes.c_int),
+        ("counters", ctypes.c_void_p), ("kind", ctypes.c_int), ("tile_n", ctypes.c_int),
     ]
 
 
@@ -115,7 +115,7 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.ts_abi_version() != 1:
+    if lib.ts_abi_version() != 2:
         raise RuntimeError("libtilesync_b200.so ABI version mismatch")
     _lib = lib
     return lib

@@ -26,7 +26,8 @@ class MlpChain:
                  reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0,
                  extra_flags: int = 0, cta_group: int = 2, prod_order: TileOrder = RowMajor(),
                  cons_order: TileOrder = RowMajor(), swap_ab: bool = False,
-                 prod_splits: int = 1, cons_splits: int = 1):
+                 prod_splits: int = 1, cons_splits: int = 1, prod_tile_n: int = 0,
+                 cons_tile_n: int = 0):
         m = x.shape[0]
         self.x, self.w1, self.w2 = x, w1, w2
         self.h = torch.empty(m, w1.shape[0], dtype=x.dtype, device=x.device)
@@ -35,9 +36,9 @@ class MlpChain:
                          num_ctas=num_ctas, extra_flags=extra_flags, cta_group=cta_group,
                          swap_ab=swap_ab)
         self.prod = self.cs.stage(x, w1, self.h, epilogue="gelu", order=prod_order, id="gemm1",
-                                  splits=prod_splits)
+                                  splits=prod_splits, tile_n=prod_tile_n)
         self.cons = self.cs.stage(self.h, w2, self.y, order=cons_order, id="gemm2",
-                                  splits=cons_splits)
+                                  splits=cons_splits, tile_n=cons_tile_n)
         self.dep = self.cs.dependency(policy, self.prod, self.cons, operand="a")
 
     def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
@@ -69,15 +70,18 @@ class SwigluChain:
     def __init__(self, x: torch.Tensor, w_gate_up: torch.Tensor, w_down: torch.Tensor,
                  policy: SyncPolicy = RowSync(), mode: str = "fused", tile_n: int = 256,
                  reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0,
-                 cta_group: int = 2):
+                 cta_group: int = 2, prod_tile_n: int = 0, cons_tile_n: int = 0):
+        """``prod_tile_n`` = 512 packs gate/up per 512-row block
+        (``interleave_gate_up(wg, wu, 512)``)."""
         m = x.shape[0]
         f = w_gate_up.shape[0] // 2
         self.h = torch.empty(m, f, dtype=x.dtype, device=x.device)
         self.y = torch.empty(m, w_down.shape[0], dtype=x.dtype, device=x.device)
         self.cs = CuSync(tile_n=tile_n, mode=mode, reorder=reorder, keep_sems=keep_sems,
                          num_ctas=num_ctas, cta_group=cta_group)
-        self.prod = self.cs.stage(x, w_gate_up, self.h, epilogue="swiglu", id="gate_up")
-        self.cons = self.cs.stage(self.h, w_down, self.y, id="down")
+        self.prod = self.cs.stage(x, w_gate_up, self.h, epilogue="swiglu", id="gate_up",
+                                  tile_n=prod_tile_n)
+        self.cons = self.cs.stage(self.h, w_down, self.y, id="down", tile_n=cons_tile_n)
         self.dep = self.cs.dependency(policy, self.prod, self.cons, operand="a")
 
     def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:

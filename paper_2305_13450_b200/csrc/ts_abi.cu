@@ -93,7 +93,7 @@ int launch_one(const ts::ChainParams& p, int units, cudaStream_t stream) {
   if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG, 1, 1);
-  cfg.blockDim = dim3(ts::kThreads, 1, 1);
+  cfg.blockDim = dim3(C::kThreads, 1, 1);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -151,11 +151,20 @@ int cta_group_of(const ts_chain_desc* d) {
   return d->cta_group == 0 ? 2 : d->cta_group;
 }
 
+// 1 if GeMM stage `st` uses double-width CTA-pair tiles (ts_stage_desc.tile_n = 512),
+// 0 for the chain's tile width, -1 if its tile_n is not allowed.
+int stage_wide(const ts_stage_desc& st, int bn, int cg, int swap) {
+  if (st.tile_n == 0 || st.tile_n == (swap ? 128 : bn)) return 0;
+  if (st.kind == TS_STAGE_GEMM && !swap && cg == 2 && bn == 256 && st.tile_n == 512) return 1;
+  return -1;
+}
+
 // Output columns one tile of stage `st` writes (the producer "column tile" width that a
 // consumer k-step covers).
-int out_tile_cols(const ts_stage_desc& st, int bn, int swap) {
+int out_tile_cols(const ts_stage_desc& st, int bn, int cg, int swap) {
   if (swap) return 128;
-  return st.epilogue == TS_EPI_SWIGLU ? bn / 2 : bn;
+  const int w = stage_wide(st, bn, cg, swap) > 0 ? 2 * bn : bn;
+  return st.epilogue == TS_EPI_SWIGLU ? w / 2 : w;
 }
 
 // Validate the descriptor and fill kernel parameters (everything but tensor maps when
@@ -205,6 +214,8 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       if (st.lda < 3 * st.n || st.lda % 8 || st.ldc < st.n || st.ldc % 8)
         return fail(TS_ERR_VALUE, "stage %d: dot needs lda >= 3n and ldc >= n (multiples of 8)", s);
       if (!st.a || !st.c) return fail(TS_ERR_VALUE, "stage %d: null operand pointer", s);
+      if (st.tile_n != 0 && st.tile_n != bn)
+        return fail(TS_ERR_CONFIG, "stage %d: the dot stage uses the chain's tile width", s);
       if ((reinterpret_cast<uintptr_t>(st.a) | reinterpret_cast<uintptr_t>(st.c)) & 15)
         return fail(TS_ERR_VALUE, "stage %d: operands must be 16-byte aligned", s);
       if (st.order != TS_ORDER_ROW_MAJOR && st.order != TS_ORDER_BANDED_COLUMN_MAJOR)
@@ -239,9 +250,14 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       return fail(TS_ERR_CONFIG, "stage %d: the SwiGLU epilogue needs the normal tile layout", s);
     if (st.m < 1 || st.n < 1 || st.k < 1)
       return fail(TS_ERR_VALUE, "stage %d: m, n, k must be >= 1", s);
-    if (st.n % tile_n != 0)
+    const int wide = stage_wide(st, bn, cg, swap);
+    if (wide < 0)
+      return fail(TS_ERR_CONFIG, "stage %d: tile_n %d unsupported (0, %d, or 512 with cta_group 2 "
+                  "and chain tile_n 256)", s, st.tile_n, tile_n);
+    const int stage_tile_n = tile_n << wide;
+    if (st.n % stage_tile_n != 0)
       return fail(TS_ERR_CONFIG, "stage %d: n=%d is not a multiple of the tile width %d", s, st.n,
-                  tile_n);
+                  stage_tile_n);
     const int splits = st.splits < 1 ? 1 : st.splits;
     if (st.k % (ts::kBK * splits) != 0)
       return fail(TS_ERR_CONFIG, "stage %d: k=%d is not a multiple of %d x %d split(s)", s, st.k,
@@ -263,7 +279,8 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.k = st.k;
     sp.ldc = st.ldc;
     sp.grid_x = (st.m + tile_m - 1) / tile_m;
-    sp.grid_y = st.n / tile_n;
+    sp.grid_y = st.n / stage_tile_n;
+    sp.wide = wide;
     sp.splits = splits;
     sp.ws = st.workspace;
     sp.cnt = st.counters;
@@ -318,7 +335,9 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
                   cs.grid_x, ps.grid_x);
     if (cs.in_dep >= 0)
       return fail(TS_ERR_CONFIG, "dependency %d: stage %d already has an operand-A dependency", i, dd.consumer);
-    const int cols = ps.kind == ts::kStageDot ? bn : out_tile_cols(d->stages[dd.producer], bn, swap);
+    if (cs.kind == ts::kStageDot && ps.wide)
+      return fail(TS_ERR_CONFIG, "dependency %d: a stage feeding the dot stage must use the chain's tile width", i);
+    const int cols = ps.kind == ts::kStageDot ? bn : out_tile_cols(d->stages[dd.producer], bn, cg, swap);
     int kb_per_kstep = cols / ts::kBK;
     int k_steps = 0;
     if (cs.kind == ts::kStageDot) {

@@ -37,12 +37,25 @@
 namespace ts {
 
 constexpr int kBK = 64;         // K elements per smem stage = one 128-B swizzle row
-constexpr int kThreads = 256;
 constexpr int kTileRing = 4;    // tile-id hand-off ring between scheduler and consumers
-constexpr int kEpiThreads = 128;
+// Operand pipeline barriers are indexed by K-block sequence number (full: TMA bytes
+// landed) and by commit group (empty: the MMAs that read a group of K-blocks are done),
+// not by smem ring entry. One tcgen05.commit then frees several K-blocks (measured: each
+// commit costs the tensor pipe a drain bubble), and the ring geometry (fixed slots or
+// 16-KB chunks, 1-3 per K-block) is independent of the barriers.
+constexpr int kFullRing = 16;    // > K-blocks in flight (<= 13)
+constexpr int kCommitRing = 16;  // > commit groups in flight
 constexpr uint64_t kWatchdogNs = 4000000000ull;
 constexpr int kStageGemm = 0;  // C = epi(A x B^T) on tcgen05
 constexpr int kStageDot = 1;   // attention's fused softmax-dot over QKV column tiles
+
+// K-blocks per tcgen05.commit (flags bits 17-18: 1 -> 1, 2 -> 2, 3 -> 4; 0 -> default 2).
+__host__ __device__ __forceinline__ int commit_group(int flags) {
+  const int g = (flags >> 17) & 3;
+  return g ? 1 << (g - 1) : 2;
+}
+// Ring-entry counter step without a division.
+__device__ __forceinline__ int wrap_inc(int e, int n) { return e + 1 == n ? 0 : e + 1; }
 
 struct StageParams {
   CUtensorMap tmap_a;  // activations [m, k] K-major, 128-B swizzle
@@ -68,6 +81,7 @@ struct StageParams {
   // right away. `dot_dep` is this (producer) stage's dependency into such a dot stage.
   int dot_dep;       // producer side: dependency index, or -1
   int last_arriver;  // dot side: 1 when its tiles run on the last-arriving producer
+  int wide;          // 1: double-width pair tile (2 x BN output columns, Cfg::kChunked)
 };
 
 struct DepParams {
@@ -96,6 +110,22 @@ struct ChainParams {
 // smem byte of the dominant operand is weight — the HBM-bound regime.
 template <int BN, int CG, bool SW = false>
 struct Cfg {
+  // CTA-pair 256-wide tiles stage operands through a ring of 16-KB chunks (one 128-row
+  // x 64-K box each) instead of fixed slots, so a stage can use double-width tiles
+  // (A + two B boxes per K-block, 256 x 512 outputs per pair): 25 % fewer operand bytes
+  // per MAC, which is what bounds the 256 x 256 tile (L2 -> SM operand bandwidth).
+  static constexpr bool kChunked = CG == 2 && BN == 256 && !SW;
+  // Epilogue warps: 4 (one per TMEM lane quarter), or 8 for chunked tiles (two column
+  // groups per lane quarter: a 256 x 512 tile's accumulator is single-buffered, so its
+  // drain is on the MMA warp's critical path).
+  static constexpr int kEpiGroups = kChunked ? 2 : 1;
+  static constexpr int kEpiThreads = 128 * kEpiGroups;
+  static constexpr int kThreads = 128 + kEpiThreads;
+  static constexpr int kChunkBytes = 16384;
+  // A boxes and B boxes live in separate chunk rings (A ring first in smem)
+  static constexpr int kAChunks = 6;
+  static constexpr int kBChunks = 8;
+  static constexpr int kChunks = kAChunks + kBChunks;
   static constexpr int kTileM = SW ? BN : 128 * CG;  // activation rows of a tile
   static constexpr int kTileN = SW ? 128 : BN;       // output columns of a tile
   static constexpr int kBRows = SW ? BN : BN / CG;   // rows of the UMMA-N operand per CTA
@@ -111,11 +141,14 @@ struct Cfg {
   static constexpr int kAcc = SW ? (BN >= 256 ? 1 : 256 / BN > 8 ? 8 : 256 / BN) : 1;
   static constexpr int kAccCols = kAcc * BN;           // TMEM columns of one tile buffer
   static constexpr int kTmemCols = 2 * kAccCols;       // two tile buffers
-  static constexpr int kBarOffset = kStages * kStageBytes;
-  // full, empty per stage; tmem full/empty x2; tile ring full/empty; peer_done x2
-  static constexpr int kNumBars = 2 * kStages + 4 + 2 * kTileRing + 2;
+  static constexpr int kRing = kChunked ? kChunks : kStages;  // ring entries
+  static constexpr int kBarOffset = kChunked ? kChunks * kChunkBytes : kStages * kStageBytes;
+  // K-block full, commit-group empty; tmem full/empty x2; tile ring full/empty; peer_done x2
+  static constexpr int kNumBars = kFullRing + kCommitRing + 4 + 2 * kTileRing + 2;
   // + tile ring ids, TMEM slot, flags and the last-arriver dot list (64 ints)
-  static constexpr int kSmemBytes = 1024 + kBarOffset + kNumBars * 8 + 64 + 272;
+  // + tile ring ids, TMEM slot, flags and the last-arriver dot list (64 ints), ring-entry
+  // owners (commit group that last read each entry)
+  static constexpr int kSmemBytes = 1024 + kBarOffset + kNumBars * 8 + 64 + 272 + 4 * kRing;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
   static_assert(kBRows % 8 == 0 && kBRows <= 256, "B box rows");
 };
@@ -161,8 +194,14 @@ struct AbFormat<__nv_bfloat16> {
   static constexpr uint32_t value = 1;
 };
 
-__device__ __forceinline__ float gelu_erf(float x) {
-  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+// GeLU in GPT-3's tanh form (GPT-2/3 "gelu_new"), with the hardware
+// tanh: 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))).
+__device__ __forceinline__ float gelu(float x) {
+  const float u = x * fmaf(0.0356774081f, x * x, 0.7978845608f);
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  const float hx = 0.5f * x;
+  return fmaf(hx, t, hx);
 }
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
@@ -272,6 +311,19 @@ struct Tile {
   int g, s, tb, tx, ty, tz;
 };
 
+// 32 packed 16-bit outputs (64 B) of one row: two 256-bit stores, or four 128-bit ones.
+template <typename T>
+__device__ __forceinline__ void store_row32(T* dst, const uint32_t (&pk)[16], bool v8ok) {
+  if (v8ok) {
+    ptx::st_global_v8(dst, pk);
+    ptx::st_global_v8(dst + 16, pk + 8);
+  } else {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+  }
+}
+
 __device__ __forceinline__ Tile decode(const ChainParams& p, int g) {
   Tile t;
   t.g = g;
@@ -284,19 +336,23 @@ __device__ __forceinline__ Tile decode(const ChainParams& p, int g) {
 }
 
 template <int BN, int CG, typename T, bool SW>
-__global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constant__ ChainParams p) {
+__global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
+    chain_kernel(const __grid_constant__ ChainParams p) {
   using C = Cfg<BN, CG, SW>;
+  constexpr int kEpiThreads = C::kEpiThreads;
+  constexpr int kEpiWarps = kEpiThreads / 32;
   static_assert(!SW || CG == 1, "swapped tiles use single-CTA MMAs");
   constexpr int S = C::kStages;
+  constexpr int R = C::kRing;  // smem ring entries (slots, or chunks when kChunked)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;                       // S x [128 x 64]
   uint8_t* sB = smem + S * C::kABytes;      // S x [BN/CG x 64]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOffset);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + S;
-  uint64_t* tmem_full = bars + 2 * S;
+  uint64_t* full = bars;               // [kFullRing], by K-block sequence number
+  uint64_t* empty = bars + kFullRing;  // [kCommitRing], by commit group
+  uint64_t* tmem_full = empty + kCommitRing;
   uint64_t* tmem_empty = tmem_full + 2;
   uint64_t* ti_full = tmem_empty + 2;
   uint64_t* ti_empty = ti_full + kTileRing;
@@ -307,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
   int* split_flag = last_flag + 1;
   int* dot_count = split_flag + 1;  // last-arriver dot tiles released by a post
   int* dot_list = dot_count + 1;    // [0, 32): dot tile columns, [32, 64): their tb
+  int* owner = dot_list + 64;       // [R]: commit group that last read each ring entry
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -314,19 +371,18 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
   const bool leader = rank == 0;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < S; ++i) {
-      ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&empty[i], 1);
-    }
+    for (int i = 0; i < kFullRing; ++i) ptx::mbar_init(&full[i], 1);
+    for (int i = 0; i < kCommitRing; ++i) ptx::mbar_init(&empty[i], 1);
+    for (int i = 0; i < R; ++i) owner[i] = -1;
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tmem_full[i], 1);
-      ptx::mbar_init(&tmem_empty[i], CG * kEpiThreads / 32);
+      ptx::mbar_init(&tmem_empty[i], CG * kEpiWarps);
       ptx::mbar_init(&peer_done[i], 1);
     }
     for (int i = 0; i < kTileRing; ++i) {
       ptx::mbar_init(&ti_full[i], 1);
       // leader MMA warp + every epilogue warp of the pair + the peer's producer lane
-      ptx::mbar_init(&ti_empty[i], 1 + CG * kEpiThreads / 32 + (CG - 1));
+      ptx::mbar_init(&ti_empty[i], 1 + CG * kEpiWarps + (CG - 1));
     }
     *dot_count = 0;
     ptx::fence_barrier_init();
@@ -379,11 +435,21 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
       const uint64_t pol_normal = ptx::policy_evict_normal();
       const uint64_t pol_last = ptx::policy_evict_last();
       const int b_hint = (p.flags >> 8) & 3;
-      uint32_t full_cluster[S];
-      if constexpr (CG == 2) {
-        for (int i = 0; i < S; ++i) full_cluster[i] = ptx::mapa(&full[i], 0);
-      }
-      uint32_t pipe = 0;
+      // ring entries: ea = next A entry (slot, or A chunk), eb = next B chunk (chunked)
+      int ea = 0, eb = C::kChunked ? C::kAChunks : 0;
+      uint32_t kq = 0;    // K-blocks issued (full barrier index)
+      uint32_t cid = 0;   // commit group of the K-block being issued
+      const int group = commit_group(p.flags);
+      // Claim ring entry e for commit group `cid` once the MMAs of the group that last
+      // read it are done.
+      auto claim = [&](int e) {
+        const int o = owner[e];
+        if (o >= 0) {
+          const uint32_t uo = static_cast<uint32_t>(o);
+          ptx::mbar_wait(&empty[uo % kCommitRing], (uo / kCommitRing) & 1);
+        }
+        owner[e] = static_cast<int>(cid);
+      };
 #pragma unroll 1
       for (int it = 0;; ++it) {
         int g;
@@ -415,7 +481,10 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         if (st.kind == kStageDot) continue;  // pointwise stage: the epilogue warps run it
         // activation (dependent) and weight (independent) tile rows of this CTA
         const int act_row = SW ? t.tx * BN : t.tx * C::kTileM + static_cast<int>(rank) * 128;
-        const int w_row = SW ? t.ty * 128 : t.ty * BN + static_cast<int>(rank) * C::kBRows;
+        // a double-width tile's second B box (output columns [BN, 2 BN) of the pair
+        // tile) starts BN weight rows further; each CTA holds its 128-row half of both
+        const int wide = C::kChunked ? st.wide : 0;
+        const int w_row = SW ? t.ty * 128 : t.ty * (BN << wide) + static_cast<int>(rank) * C::kBRows;
         const int d = st.in_dep;
         const int bh = b_hint ? b_hint : (st.grid_x == 1 ? 1 : 2);
         const uint64_t pol_b = bh == 1 ? pol_first : (bh == 2 ? pol_normal : pol_last);
@@ -461,36 +530,68 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
           for (int ks = 0; ks * kbpk < kb_begin; ++ks) wait_kstep(ks);
         }
 #pragma unroll 1
-        for (int i = 0; i < k_per; ++i, ++pipe) {
-          const int kb = kb_begin + (i + rot) % k_per;
-          const int rs = pipe % S;
-          ptx::mbar_wait(&empty[rs], ((pipe / S) & 1) ^ 1);
+        for (int i = 0, kb = kb_begin + rot, gi = 0; i < k_per; ++i) {
           // diagnostic only (flag bit 15): stream the weights, skip the activation loads
           const bool skip_act = (p.flags >> 15) & 1;
-          if (leader)
-            ptx::mbar_arrive_expect_tx(&full[rs],
-                                       CG * (skip_act ? (SW ? C::kABytes : C::kBBytes)
-                                                      : C::kStageBytes));
-          // normal layout: activations -> UMMA-M operand (sA), weights -> UMMA-N (sB);
-          // swapped layout: weights -> sA, activations -> sB
-          uint8_t* act_dst = SW ? sB + rs * C::kBBytes : sA + rs * C::kABytes;
-          uint8_t* w_dst = SW ? sA + rs * C::kABytes : sB + rs * C::kBBytes;
+          // normal layout: activations -> UMMA-M operand, weights -> UMMA-N; swapped:
+          // weights -> UMMA-M, activations -> UMMA-N. Chunked: one A chunk, 1-2 B chunks.
+          const int e0 = ea;
+          claim(e0);
+          ea = wrap_inc(ea, C::kChunked ? C::kAChunks : R);
+          int e1 = 0, e2 = 0;
+          if constexpr (C::kChunked) {
+            e1 = eb;
+            claim(e1);
+            eb = eb + 1 == R ? C::kAChunks : eb + 1;
+            if (wide) {
+              e2 = eb;
+              claim(e2);
+              eb = eb + 1 == R ? C::kAChunks : eb + 1;
+            }
+          }
+          uint64_t* fb = &full[kq % kFullRing];
+          const uint32_t fbc = CG == 2 ? ptx::mapa(fb, 0) : 0;  // the leader CTA's barrier
+          if (leader) {
+            const int nc = 2 + wide;
+            const int bytes = C::kChunked ? C::kChunkBytes * (skip_act ? nc - 1 : nc)
+                                          : (skip_act ? (SW ? C::kABytes : C::kBBytes)
+                                                      : C::kStageBytes);
+            ptx::mbar_arrive_expect_tx(fb, CG * bytes);
+          }
+          uint8_t* act_dst;
+          uint8_t* w_dst;
+          if constexpr (C::kChunked) {
+            act_dst = smem + e0 * C::kChunkBytes;
+            w_dst = smem + e1 * C::kChunkBytes;
+          } else {
+            act_dst = SW ? sB + e0 * C::kBBytes : sA + e0 * C::kABytes;
+            w_dst = SW ? sA + e0 * C::kABytes : sB + e0 * C::kBBytes;
+          }
           auto load_b = [&]() {
             if constexpr (CG == 2) {
-              ptx::tma_load_2d_pair(w_dst, &st.tmap_b, full_cluster[rs], kb * kBK, w_row, pol_b);
+              ptx::tma_load_2d_pair(w_dst, &st.tmap_b, fbc, kb * kBK, w_row, pol_b);
+              if (C::kChunked && wide)
+                ptx::tma_load_2d_pair(smem + e2 * C::kChunkBytes, &st.tmap_b, fbc, kb * kBK,
+                                      w_row + BN, pol_b);
             } else {
-              ptx::tma_load_2d(w_dst, &st.tmap_b, &full[rs], kb * kBK, w_row, pol_b);
+              ptx::tma_load_2d(w_dst, &st.tmap_b, fb, kb * kBK, w_row, pol_b);
             }
           };
           if (reorder) load_b();
           if (waits && rot == 0 && kb % kbpk == 0) wait_kstep(kb / kbpk);
           if (skip_act) {
           } else if constexpr (CG == 2) {
-            ptx::tma_load_2d_pair(act_dst, &st.tmap_a, full_cluster[rs], kb * kBK, act_row, pol_a);
+            ptx::tma_load_2d_pair(act_dst, &st.tmap_a, fbc, kb * kBK, act_row, pol_a);
           } else {
-            ptx::tma_load_2d(act_dst, &st.tmap_a, &full[rs], kb * kBK, act_row, pol_a);
+            ptx::tma_load_2d(act_dst, &st.tmap_a, fb, kb * kBK, act_row, pol_a);
           }
           if (!reorder) load_b();
+          ++kq;
+          if (++gi == group || i + 1 == k_per) {  // the K-block closes a commit group
+            ++cid;
+            gi = 0;
+          }
+          if (++kb == kb_end) kb = kb_begin;
         }
         // ... and the ones after it once its loads are issued.
         if (waits && rot == 0)
@@ -502,8 +603,11 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
     if (leader) {
       // UMMA shape: M = 128 per CTA (256 for a pair), N = BN in both layouts
       constexpr uint32_t kIdesc = ptx::idesc_f16(128 * CG, BN, AbFormat<T>::value);
-      uint32_t pipe = 0;
-      uint32_t local = 0;
+      int ea = 0, eb = C::kChunked ? C::kAChunks : 0;  // ring entries, as the producer
+      uint32_t kq = 0;    // K-blocks consumed (full barrier index)
+      uint32_t cid = 0;   // commit group
+      const int group = commit_group(p.flags);
+      uint32_t u = 0;  // TMEM accumulator-slot uses (a double-width tile takes two)
 #pragma unroll 1
       for (int it = 0;; ++it) {
         const int g = ring_take(it, false);
@@ -511,66 +615,90 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         const StageParams& sp = p.st[stage_of(p, g)];
         if (sp.kind == kStageDot) continue;  // no MMA, no accumulator buffer
         const int kblocks = sp.k_blocks / sp.splits;
-        const uint32_t acc = local & 1;
-        if constexpr (CG == 2) {
-          // TMEM reuse only; tcgen05 fences order the peer's loads before this MMA
-          ptx::mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
-        } else {
-          ptx::mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
-        }
+        const int wide = C::kChunked ? sp.wide : 0;
+        // TMEM reuse only (for pairs, tcgen05 fences order the peer's loads)
+        for (int j = 0; j <= wide; ++j)
+          ptx::mbar_wait(&tmem_empty[(u + j) & 1], (((u + j) >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
+        const uint32_t d_tmem = tmem_base + (u & 1) * C::kAccCols;
+        const uint32_t d_tmem2 = tmem_base + ((u + 1) & 1) * C::kAccCols;
         const bool tr = p.trace != nullptr;
+        const bool no_mma = (p.flags >> 13) & 1;  // diagnostic only: skip the MMAs
         uint64_t starve_ns = 0;  // time this tile's MMAs waited for operand stages
 #pragma unroll 1
-        for (int kb = 0; kb < kblocks; ++kb, ++pipe) {
-          const int rs = pipe % S;
-          if (tr && !ptx::mbar_test_wait(&full[rs], (pipe / S) & 1)) {
+        for (int kb = 0, gi = 0; kb < kblocks; ++kb) {
+          uint64_t* fb = &full[kq % kFullRing];
+          const uint32_t ph = (kq / kFullRing) & 1;
+          if (tr && !ptx::mbar_test_wait(fb, ph)) {
             const uint64_t t0 = ptx::global_timer();
-            ptx::mbar_wait(&full[rs], (pipe / S) & 1);
+            ptx::mbar_wait(fb, ph);
             if (kb > 0) starve_ns += ptx::global_timer() - t0;
           } else {
-            ptx::mbar_wait(&full[rs], (pipe / S) & 1);
+            ptx::mbar_wait(fb, ph);
           }
           if (tr && kb == 0 && lane == 0) {
             const Tile t = decode(p, g);
             trace_event(p, ptx::global_timer(), 5, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty);
           }
           ptx::tc_fence_after();
-          if ((p.flags >> 13) & 1) {  // diagnostic only: stream operands, skip the MMAs
-            if (lane == 0) ptx::mbar_arrive(&empty[rs]);
-            __syncwarp();
-            continue;
-          }
           if (lane == 0) {
-            const uint32_t a_addr = ptx::smem_u32(sA + rs * C::kABytes);
-            const uint32_t b_addr = ptx::smem_u32(sB + rs * C::kBBytes);
-            if constexpr (C::kAcc > 1) {
-#pragma unroll
-              for (int k = 0; k < kBK / 16; ++k) {
-                const uint64_t ad = ptx::smem_desc_k_sw128(a_addr + k * 32);
-                const uint64_t bd = ptx::smem_desc_k_sw128(b_addr + k * 32);
-                const int step = kb * (kBK / 16) + k;  // rotate independent accumulators
-                ptx::umma_f16(d_tmem + (step % C::kAcc) * BN, ad, bd, kIdesc, step >= C::kAcc);
+            if constexpr (C::kChunked) {
+              // A chunk; B chunk(s): output columns [0, BN) and, double width, [BN, 2 BN)
+              auto desc = [&](int e) {
+                return ptx::smem_desc_k_sw128(ptx::smem_u32(smem + e * C::kChunkBytes));
+              };
+              const uint64_t ad = desc(ea);
+              const int eb2 = eb + 1 == R ? C::kAChunks : eb + 1;
+              if (!no_mma) {
+                ptx::umma_f16_kblock<CG>(d_tmem, ad, desc(eb), kIdesc, kb != 0);
+                if (wide) ptx::umma_f16_kblock<CG>(d_tmem2, ad, desc(eb2), kIdesc, kb != 0);
               }
             } else {
-              // the K-block's four MMAs back to back in one issue sequence
-              ptx::umma_f16_kblock<CG>(d_tmem, ptx::smem_desc_k_sw128(a_addr),
-                                       ptx::smem_desc_k_sw128(b_addr), kIdesc, kb != 0);
+              const int rs = ea;
+              const uint32_t a_addr = ptx::smem_u32(sA + rs * C::kABytes);
+              const uint32_t b_addr = ptx::smem_u32(sB + rs * C::kBBytes);
+              if (no_mma) {
+              } else if constexpr (C::kAcc > 1) {
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k) {
+                  const uint64_t ad = ptx::smem_desc_k_sw128(a_addr + k * 32);
+                  const uint64_t bd = ptx::smem_desc_k_sw128(b_addr + k * 32);
+                  const int step = kb * (kBK / 16) + k;  // rotate independent accumulators
+                  ptx::umma_f16(d_tmem + (step % C::kAcc) * BN, ad, bd, kIdesc, step >= C::kAcc);
+                }
+              } else {
+                // the K-block's four MMAs back to back in one issue sequence
+                ptx::umma_f16_kblock<CG>(d_tmem, ptx::smem_desc_k_sw128(a_addr),
+                                         ptx::smem_desc_k_sw128(b_addr), kIdesc, kb != 0);
+              }
             }
-            if constexpr (CG == 2) {
-              ptx::umma_commit_pair(&empty[rs]);
-            } else {
-              ptx::umma_commit(&empty[rs]);
+            // one commit frees every ring entry of the group's K-blocks
+            if (gi + 1 == group || kb + 1 == kblocks) {
+              if constexpr (CG == 2) {
+                ptx::umma_commit_pair(&empty[cid % kCommitRing]);
+              } else {
+                ptx::umma_commit(&empty[cid % kCommitRing]);
+              }
             }
           }
+          if (++gi == group || kb + 1 == kblocks) {
+            ++cid;
+            gi = 0;
+          }
+          ea = wrap_inc(ea, C::kChunked ? C::kAChunks : R);
+          if constexpr (C::kChunked) {
+            for (int c = 0; c <= wide; ++c) eb = eb + 1 == R ? C::kAChunks : eb + 1;
+          }
+          ++kq;
           __syncwarp();
         }
         if (lane == 0) {
-          if constexpr (CG == 2) {
-            ptx::umma_commit_pair(&tmem_full[acc]);
-          } else {
-            ptx::umma_commit(&tmem_full[acc]);
+          for (int j = 0; j <= wide; ++j) {
+            if constexpr (CG == 2) {
+              ptx::umma_commit_pair(&tmem_full[(u + j) & 1]);
+            } else {
+              ptx::umma_commit(&tmem_full[(u + j) & 1]);
+            }
           }
           if (tr) {
             const Tile t = decode(p, g);
@@ -580,13 +708,15 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
           }
         }
         __syncwarp();
-        ++local;
+        u += 1 + wide;
       }
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
-    const int ew = warp - 4;  // == warp % 4: TMEM lanes [32*ew, 32*ew+32)
-    uint32_t local = 0;
+    const int ew = warp & 3;         // TMEM lanes [32*ew, 32*ew+32) (a warp's lane quarter)
+    const int eg = (warp - 4) >> 2;  // column group (chunked tiles: 0 or 1)
+    uint32_t local = 0;  // GeMM tiles (peer_done parity)
+    uint32_t u = 0;      // TMEM accumulator-slot uses, as counted by the MMA warp
     uint32_t tmem_empty_remote[2] = {0, 0}, peer_done_remote[2] = {0, 0};
     if constexpr (CG == 2) {
       if (!leader) {
@@ -603,7 +733,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
       ptx::fence_acq_rel_gpu();
 #pragma unroll 1
-      for (int rr = ew * 32 + lane; rr < C::kTileM; rr += kEpiThreads) {
+      for (int rr = (warp - 4) * 32 + lane; rr < C::kTileM; rr += kEpiThreads) {
         const int row = tx * C::kTileM + rr;
         if (row < sd.m) {
           // a dot tile covers BN / 128 heads (the paper's stride H / (8 Ty))
@@ -654,23 +784,31 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         continue;
       }
       const uint32_t acc = local & 1;
-      if constexpr (CG == 2) {
-        ptx::mbar_wait(&tmem_full[acc], (local >> 1) & 1);  // arrived by the MMA commit
-      } else {
-        ptx::mbar_wait(&tmem_full[acc], (local >> 1) & 1);
-      }
+      const int wide = C::kChunked ? st.wide : 0;
+      for (int j = 0; j <= wide; ++j)  // arrived by the MMA commits
+        ptx::mbar_wait(&tmem_full[(u + j) & 1], ((u + j) >> 1) & 1);
       ptx::tc_fence_after();
-      const uint32_t t_lane =
-          tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * C::kAccCols;
-      auto release_tmem = [&]() {
+      if (threadIdx.x == 128 && leader && p.trace != nullptr)  // epilogue begin (extension)
+        trace_event(p, ptx::global_timer(), 7, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
+      const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
+      const uint32_t t_lane = lane_base + (u & 1) * C::kAccCols;
+      // accumulator column x of this tile (a double-width tile spans both slots)
+      auto tcol = [&](int x) -> uint32_t {
+        return lane_base + ((u + x / BN) & 1) * C::kAccCols + (x % BN);
+      };
+      auto release_slot = [&](int j) {
         ptx::tc_fence_before();
         if (lane == 0) {
+          const uint32_t sl = (u + j) & 1;
           if (CG == 2 && !leader) {
-            ptx::mbar_arrive_remote(tmem_empty_remote[acc]);
+            ptx::mbar_arrive_remote(tmem_empty_remote[sl]);
           } else {
-            ptx::mbar_arrive(&tmem_empty[acc]);
+            ptx::mbar_arrive(&tmem_empty[sl]);
           }
         }
+      };
+      auto release_tmem = [&]() {
+        for (int j = 0; j <= wide; ++j) release_slot(j);
       };
       if constexpr (SW) {
         // Swapped tile: TMEM lane = output column, TMEM column = activation row.
@@ -678,7 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         const int ncol = t.ty * 128 + ncl;
         const int b0 = t.tx * BN;
         const int rows = st.m - b0 < BN ? st.m - b0 : BN;
-        const bool gelu = st.epilogue == TS_EPI_GELU;
+        const bool gl = st.epilogue == TS_EPI_GELU;
         T* cout = reinterpret_cast<T*>(st.c) + ncol;
         // accumulators the MMA warp actually wrote (fewer than kAcc for very short K)
         const int steps = (st.k_blocks / st.splits) * (kBK / 16);
@@ -707,7 +845,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int b = cc * 32 + j;
-              const float o = gelu ? gelu_erf(v[j]) : v[j];
+              const float o = gl ? gelu(v[j]) : v[j];
               if (b < rows) cout[static_cast<size_t>(b0 + b) * st.ldc] = to_elem<T>(o);
             }
           }
@@ -756,7 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 if (b8 + j < rows) {
-                  const float o = gelu ? gelu_erf(s[j]) : s[j];
+                  const float o = gl ? gelu(s[j]) : s[j];
                   cout[static_cast<size_t>(b0 + b8 + j) * st.ldc] = to_elem<T>(o);
                 }
               }
@@ -767,13 +905,22 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
       const int row = t.tx * C::kTileM + static_cast<int>(rank) * 128 + ew * 32 + lane;
       const bool row_ok = row < st.m;
       T* crow = reinterpret_cast<T*>(st.c) + static_cast<size_t>(row) * st.ldc;
+      const int acc_cols = BN << wide;  // accumulator columns of this tile
+      // full-sector (32-B) stores when the output rows are 32-B aligned
+      const bool v8ok = ((reinterpret_cast<uintptr_t>(st.c) | (st.ldc * sizeof(T))) & 31) == 0;
+      constexpr int G = C::kEpiGroups;
       if (st.epilogue == TS_EPI_SWIGLU) {
-        T* out = crow + t.ty * (BN / 2);
+        // gate = accumulator columns [0, acc_cols/2), up = the matching upper half; each
+        // column group stores its 1/G of the output columns
+        const int half = acc_cols / 2;
+        const int span = half / G;
+        T* out = crow + t.ty * half + eg * span;
 #pragma unroll 1
-        for (int cc = 0; cc < BN / 64; ++cc) {
+        for (int cc = 0; cc < span / 32; ++cc) {
+          const int x = eg * span + cc * 32;
           uint32_t gr[32], ur[32];
-          ptx::tmem_ld_32x32b_x32(t_lane + cc * 32, gr);
-          ptx::tmem_ld_32x32b_x32(t_lane + BN / 2 + cc * 32, ur);
+          ptx::tmem_ld_32x32b_x32(tcol(x), gr);
+          ptx::tmem_ld_32x32b_x32(tcol(half + x), ur);
           ptx::tmem_ld_wait();
           uint32_t pk[16];
 #pragma unroll
@@ -782,41 +929,42 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
             float u0 = __uint_as_float(ur[2 * j]), u1 = __uint_as_float(ur[2 * j + 1]);
             pk[j] = pack2<T>(silu(g0) * u0, silu(g1) * u1);
           }
-          if (row_ok) {
-            uint4* dst = reinterpret_cast<uint4*>(out + cc * 32);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-          }
+          if (row_ok) store_row32<T>(out + cc * 32, pk, v8ok);
         }
+        release_tmem();
       } else {
-        T* out = crow + t.ty * BN;
-        const bool gelu = st.epilogue == TS_EPI_GELU;
+        T* out = crow + t.ty * acc_cols;
+        const bool gl = st.epilogue == TS_EPI_GELU;
+        // Column group eg stores accumulator columns [eg * span, (eg + 1) * span); slot
+        // by slot, so a slot is handed back to the MMA warp as soon as every group is
+        // done with it (a group arrives on a slot it does not read right away).
+        const int span = acc_cols / G;
 #pragma unroll 1
-        for (int cc = 0; cc < BN / 32; ++cc) {
-          uint32_t r[32];
-          ptx::tmem_ld_32x32b_x32(t_lane + cc * 32, r);
-          ptx::tmem_ld_wait();
-          uint32_t pk[16];
+        for (int j = 0; j <= wide; ++j) {
+          const int lo = max(eg * span, j * BN), hi = min((eg + 1) * span, (j + 1) * BN);
+#pragma unroll 1
+          for (int x = lo; x < hi; x += 32) {
+            uint32_t r[32];
+            ptx::tmem_ld_32x32b_x32(tcol(x), r);
+            ptx::tmem_ld_wait();
+            uint32_t pk[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float v0 = __uint_as_float(r[2 * j]), v1 = __uint_as_float(r[2 * j + 1]);
-            if (gelu) {
-              v0 = gelu_erf(v0);
-              v1 = gelu_erf(v1);
+            for (int q = 0; q < 16; ++q) {
+              float v0 = __uint_as_float(r[2 * q]), v1 = __uint_as_float(r[2 * q + 1]);
+              if (gl) {
+                v0 = gelu(v0);
+                v1 = gelu(v1);
+              }
+              pk[q] = pack2<T>(v0, v1);
             }
-            pk[j] = pack2<T>(v0, v1);
+            if (row_ok) store_row32<T>(out + x, pk, v8ok);
           }
-          if (row_ok) {
-            uint4* dst = reinterpret_cast<uint4*>(out + cc * 32);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-          }
+          release_slot(j);
         }
       }
-      release_tmem();
       }  // normal layout
+      if (threadIdx.x == 128 && leader && p.trace != nullptr)  // epilogue stores issued
+        trace_event(p, ptx::global_timer(), 8, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
       // stage.post(): every epilogue thread's stores (of both CTAs of a pair)
       // happen-before the release below.
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
@@ -875,6 +1023,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         if (threadIdx.x == 128) *dot_count = 0;
       }
       ++local;
+      u += 1 + wide;
     }
   }
 
@@ -899,7 +1048,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
     __threadfence();
     if ((p.flags & TS_FLAG_KEEP_SEMS) == 0) {
       for (int d = 0; d < p.n_deps; ++d)
-        for (int i = threadIdx.x; i < p.dep[d].sem_n; i += kThreads) p.dep[d].sem[i] = 0;
+        for (int i = threadIdx.x; i < p.dep[d].sem_n; i += C::kThreads) p.dep[d].sem[i] = 0;
     }
     if (threadIdx.x == 0) {
       p.scratch[0] = 0;

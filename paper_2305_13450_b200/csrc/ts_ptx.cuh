@@ -210,6 +210,13 @@ __device__ __forceinline__ int atom_add_release_gpu(int* p, int v) {
   return old;
 }
 
+// 256-bit global store (sm_100: STG.256, one full 32-B sector per lane).
+__device__ __forceinline__ void st_global_v8(void* p, const uint32_t* v) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
 // ---- tcgen05 / TMEM -------------------------------------------------------------------
 template <uint32_t kCols, int CG>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {

@@ -61,6 +61,7 @@ class CuStage:
     ws: torch.Tensor | None = None
     cnt: torch.Tensor | None = None
     kind: str = "gemm"  # "gemm" or "dot" (attention's fused softmax-dot)
+    tile_n: int = 0     # 0 = the chain's tile_n; 512 = double-width CTA-pair tile
 
     @property
     def m(self) -> int:
@@ -76,18 +77,22 @@ class CuStage:
         return self.a.shape[1]
 
     @property
-    def out_tile_cols(self) -> int:
-        """Output columns one tile writes (a consumer k-step in reference units)."""
+    def width(self) -> int:
+        """Accumulator columns of one tile."""
         if self.cs.swap_ab:
             return 128
-        return self.cs.tile_n // 2 if self.epilogue == "swiglu" else self.cs.tile_n
+        return self.tile_n or self.cs.tile_n
+
+    @property
+    def out_tile_cols(self) -> int:
+        """Output columns one tile writes (a consumer k-step in reference units)."""
+        return self.width // 2 if self.epilogue == "swiglu" else self.width
 
     @property
     def grid(self) -> Dim3:
         """Tile grid as the reference's Stage.grid sees it: (activation-row tiles,
         output-column tiles, split-K slices)."""
-        cols = 128 if self.cs.swap_ab else self.cs.tile_n
-        return Dim3(-(-self.m // self.cs.tile_m), max(1, self.n // cols), self.splits)
+        return Dim3(-(-self.m // self.cs.tile_m), max(1, self.n // self.width), self.splits)
 
     def flops(self) -> int:
         return 0 if self.kind == "dot" else 2 * self.m * self.n * self.k
@@ -148,9 +153,15 @@ class CuSync:
     # -- construction ---------------------------------------------
     def stage(self, a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, epilogue: str = "none",
               order: TileOrder = RowMajor(), id: str | None = None,
-              splits: int = 1) -> CuStage:
+              splits: int = 1, tile_n: int = 0) -> CuStage:
         """Add a GeMM stage. ``splits`` > 1 splits K into that many slices (the
-        reference's z extent): each slice posts once, consumers wait for all of them."""
+        reference's z extent): each slice posts once, consumers wait for all of them.
+        ``tile_n=512`` gives this stage double-width CTA-pair tiles (256 x 512 outputs;
+        chains with ``cta_group=2, tile_n=256`` only)."""
+        if tile_n not in (0, self.tile_n) and not (
+                tile_n == 512 and self.tile_n == 256 and self.cta_group == 2 and not self.swap_ab):
+            raise ConfigError(f"stage tile_n {tile_n} unsupported (0, {self.tile_n}, or 512 "
+                              "with cta_group=2, tile_n=256)")
         if len(self.stages) >= _lib.TS_MAX_STAGES:
             raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
         if epilogue not in _EPI:
@@ -170,7 +181,7 @@ class CuSync:
         if splits < 1:
             raise ConfigError("splits must be >= 1")
         st = CuStage(self, len(self.stages), id or f"gemm{len(self.stages) + 1}", a, b, c,
-                     epilogue, order, splits)
+                     epilogue, order, splits, tile_n=tile_n)
         if splits > 1:
             tiles = st.grid.x * st.grid.y
             st.ws = torch.empty(tiles * splits * self.tile_n * 128, dtype=torch.float32,
@@ -252,6 +263,7 @@ class CuSync:
             sd.order, sd.order_stride = order_code(st.order)
             sd.splits = st.splits
             sd.kind = _lib.TS_STAGE_ATTN_DOT if st.kind == "dot" else _lib.TS_STAGE_GEMM
+            sd.tile_n = st.tile_n
             sd.workspace = st.ws.data_ptr() if st.ws is not None else None
             sd.counters = st.cnt.data_ptr() if st.cnt is not None else None
         d.n_deps = len(self.deps)

@@ -60,13 +60,21 @@ def summarize(cs, label):
             starve = [me[k].value for k in keys]
             lead = [mb[k] - start[k].t_ns for k in keys]
             # ideal tensor cycles of one tile: 4096 MAC/clk per SM (8192 per CTA pair)
-            macs = cs.tile_m * (128 if cs.swap_ab else cs.tile_n) * st.k // max(1, st.splits)
+            macs = cs.tile_m * st.width * st.k // max(1, st.splits)
             ideal = macs / (4096 * (2 if cs.cta_group == 2 else 1))
             eff = (f", {sum(cyc) / len(cyc):.0f} cycles = {ideal / (sum(cyc) / len(cyc)) * 100:.0f}%"
                    f" of the MMA floor") if cyc and st.kind == "gemm" else ""
             print(f"  {st.id}: MMA span mean {sum(mma) / len(mma) / 1e3:.1f} us{eff}, "
                   f"operand-starved {sum(starve) / len(starve) / 1e3:.1f} us, claim->first MMA "
                   f"{sum(lead) / len(lead) / 1e3:.1f} us")
+    eb = {(r.stage, r.tb): r.t_ns for r in recs if r.kind == 7}
+    ee = {(r.stage, r.tb): r.t_ns for r in recs if r.kind == 8}
+    for s_i, st in enumerate(cs.stages):
+        d = [ee[k] - eb[k] for k in eb if k[0] == s_i and k in ee]
+        lag = [eb[k] - me[k].t_ns for k in eb if k[0] == s_i and k in me]
+        if d:
+            print(f"  {st.id}: epilogue mean {sum(d) / len(d) / 1e3:.1f} us (last MMA issue -> "
+                  f"accumulator ready {sum(lag) / len(lag) / 1e3:.1f} us)")
     # MMA idle per CTA(-pair leader): before its first tile, between tiles, after its last
     per_sm = defaultdict(list)
     for k, r in me.items():
@@ -124,8 +132,10 @@ def main():
         flags = int(parts[4], 0) if len(parts) > 4 else 0
         swap_tn = int(parts[5]) if len(parts) > 5 else 0
         splits = int(parts[6]) if len(parts) > 6 else 1
+        widths = [int(w) for w in parts[7].split("/")] if len(parts) > 7 else [0, 0]
         policy = {"row": ts.RowSync(), "tile": ts.TileSync()}[pol]
-        kw = dict(swap_ab=True, tile_n=swap_tn, prod_splits=splits) if swap_tn else {}
+        kw = dict(swap_ab=True, tile_n=swap_tn, prod_splits=splits) if swap_tn else \
+            dict(prod_tile_n=widths[0], cons_tile_n=widths[1])
         ch = ts.MlpChain(x, w1, w2, policy=policy, mode=mode, prod_order=order(po),
                          cons_order=order(co), extra_flags=flags, **kw)
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)

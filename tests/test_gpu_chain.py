@@ -1,7 +1,7 @@
 """Device parity: the B200 chain kernel against the CPU oracle (oracle/tilesync_oracle.py).
 
 * numerics: within a stated fp16/bf16 tolerance of the oracle's fp32 evaluation over the
-  same rounded inputs (GeLU erf form);
+  same rounded inputs (GeLU in GPT-3's tanh form);
 * synchronization: final semaphore values, post/wait counts and the dependency-safety of
   the device trace are bit-exact against the oracle (which is pinned to the reference's
   golden vectors, tests/test_oracle_golden.py).
@@ -310,3 +310,73 @@ def test_attention_chain(m, heads, cg, mode, tn, dtype):
     if mode == "fused":
         assert {k: tuple(v) for k, v in O.final_semaphores(stages, deps).items()} == \
             ch.cs.final_semaphores()
+
+
+WIDE_CASES = [
+    # m, k, n1, n2, prod_tile_n, cons_tile_n, policy, mode
+    (256, 1024, 1024, 1024, 512, 512, ts.RowSync(), "fused"),
+    (300, 768, 1024, 512, 256, 512, ts.TileSync(), "fused"),
+    (520, 512, 512, 1024, 512, 256, ts.TileSync(), "fused"),
+    (700, 1024, 1536, 1024, 512, 512, ts.RowSync(), "stream"),
+    (64, 512, 1024, 512, 512, 256, ts.Conv2DTileSync(4), "fused"),
+]
+
+
+@pytest.mark.parametrize("m,k,n1,n2,pt,ct,pol,mode", WIDE_CASES)
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_double_width_numerics(m, k, n1, n2, pt, ct, pol, mode, dtype):
+    """Double-width CTA-pair stages (256 x 512 tiles, one A box feeding two N=256 MMAs),
+    alone and mixed with 256-wide stages in one chain."""
+    x, w1, w2 = make(m, k, n1, n2, dtype, seed=7)
+    ch = ts.MlpChain(x.cuda(), w1.cuda(), w2.cuda(), policy=pol, mode=mode, tile_n=256,
+                     cta_group=2, prod_tile_n=pt, cons_tile_n=ct)
+    for _ in range(3):
+        y = ch()
+    torch.cuda.synchronize()
+    assert not ch.cs.watchdog_fired()
+    h_ref, y_ref = oracle_mlp(x, w1, w2, dtype)
+    check_close(ch.h, h_ref, dtype)
+    check_close(y, y_ref, dtype)
+    assert all(int(v) == 0 for d in ch.cs.deps for v in d.sem.cpu())
+
+
+@pytest.mark.parametrize("pol", [ts.RowSync(), ts.TileSync()])
+@pytest.mark.parametrize("pt,ct", [(512, 512), (256, 512), (512, 256)])
+def test_double_width_trace_parity(pol, pt, ct):
+    x, w1, w2 = make(600, 512, 2048, 1024, seed=9)
+    ch = ts.MlpChain(x.cuda(), w1.cuda(), w2.cuda(), policy=pol, tile_n=256, cta_group=2,
+                     keep_sems=True, prod_tile_n=pt, cons_tile_n=ct)
+    ch.cs.enable_trace()
+    ch()
+    torch.cuda.synchronize()
+    stages, deps = _scenario_dicts(ch.cs)
+    assert stages[0]["grid"][1] == 2048 // pt and stages[1]["grid"][1] == 1024 // ct
+    evs = ch.cs.trace_events()
+    ev_dicts = [{"t": e.time, "stage": e.stage, "tb": e.tb, "kind": e.kind,
+                 "tile": list(e.tile), "k": e.k, "dep": e.dep, "sem": e.sem,
+                 "expected": e.expected} for e in evs]
+    assert O.validate_trace(ev_dicts, stages, deps, fine=True) == []
+    final = ch.cs.final_semaphores()
+    assert {k: tuple(v) for k, v in O.final_semaphores(stages, deps).items()} == final
+    dag = O.build_dep_dag(stages, deps)
+    assert sum(1 for e in evs if e.kind == "wait_end") == sum(n for (_, n) in dag.values())
+    _, y_ref = oracle_mlp(x, w1, w2, torch.float16)
+    check_close(ch.y, y_ref, torch.float16)
+
+
+def test_double_width_swiglu():
+    g = torch.Generator().manual_seed(2)
+    m, k, f, n = 300, 512, 1024, 512
+    x = torch.randn(m, k, generator=g).bfloat16()
+    wg = (torch.randn(f, k, generator=g) / k ** 0.5).bfloat16()
+    wu = (torch.randn(f, k, generator=g) / k ** 0.5).bfloat16()
+    wd = (torch.randn(n, f, generator=g) / f ** 0.5).bfloat16()
+    wgu = ts.interleave_gate_up(wg, wu, 512)
+    ch = ts.SwigluChain(x.cuda(), wgu.cuda(), wd.cuda(), policy=ts.RowSync(), tile_n=256,
+                        cta_group=2, prod_tile_n=512, cons_tile_n=512)
+    y = ch()
+    torch.cuda.synchronize()
+    h_ref, y_ref = O.swiglu_chain(x.float().numpy(), wg.float().numpy(), wu.float().numpy(),
+                                  wd.float().numpy(), "bf16")
+    check_close(ch.h, h_ref, torch.bfloat16)
+    check_close(y, y_ref, torch.bfloat16)

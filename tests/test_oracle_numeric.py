@@ -15,7 +15,7 @@ from oracle import tilesync_oracle as O
 
 def f64_mlp(x, w1, w2, dtype):
     h = x.astype(np.float64) @ w1.astype(np.float64).T
-    h = 0.5 * h * (1 + np.vectorize(math.erf)(h / math.sqrt(2)))
+    h = 0.5 * h * (1 + np.tanh(math.sqrt(2 / math.pi) * (h + 0.044715 * h ** 3)))
     h = O.round_to(h.astype(np.float32), dtype).astype(np.float64)
     return h, h @ w2.astype(np.float64).T
 
