@@ -102,7 +102,8 @@ typedef enum { TS_DTYPE_F16 = 0, TS_DTYPE_BF16 = 1 } ts_dtype;
 typedef enum {
   TS_EPI_NONE = 0,   /* C = A x B^T                                        */
   TS_EPI_GELU = 1,   /* C = GeLU_erf(A x B^T)   */
-  TS_EPI_SWIGLU = 2  /* C = SiLU(gate) * up, gate/up interleaved per tile  */
+  TS_EPI_SWIGLU = 2, /* C = SiLU(gate) * up, gate/up interleaved per tile  */
+  TS_EPI_RELU = 3    /* C = max(A x B^T, 0) (conv layers, BN folded)      */
 } ts_epilogue;
 
 typedef enum {
@@ -131,6 +132,10 @@ typedef struct {
   float* workspace;  /* splits > 1: device fp32[tiles * splits * tile_n * 128]         */
   int* counters;     /* splits > 1: device int32[tiles], zero on entry (kept zero)     */
   int kind;          /* ts_stage_kind */
+  int conv_n, conv_h, conv_w; /* TS_STAGE_CONV2D: image batch, height, width (3x3 kernel,
+                        stride 1, padding 1: output H x W = input H x W); m = n*h*w,
+                        k = 9 * Cin, a = NHWC input (lda = Cin), b = KRSC weights
+                        [n][3][3][Cin] (ldb >= 9 Cin), c = NHWC output [m, n]        */
   int tile_n;        /* this stage's tile width: 0 = the chain's tile_n; 512 = a
                         double-width CTA-pair tile (256 x 512 outputs: one A box feeds
                         two N = 256 MMAs, 25 % fewer operand bytes per MAC), allowed
@@ -139,12 +144,17 @@ typedef struct {
 } ts_stage_desc;
 
 typedef enum {
-  TS_STAGE_GEMM = 0,    /* C = epi(A x B^T) on tcgen05                                    */
-  TS_STAGE_ATTN_DOT = 1 /* attention's fused dot: a = XQKV [m, 3n] with
-                           [Q heads | K heads | V heads] 128-column head tiles, c = XDot
-                           [m, n]; XDot = Softmax(Q*V)*K per head and row (column-tile
-                           local, dropout p = 0); b unused. Tile = rows x tile_n columns
-                           (tile_n / 128 heads).                                         */
+  TS_STAGE_GEMM = 0,     /* C = epi(A x B^T) on tcgen05                                    */
+  TS_STAGE_ATTN_DOT = 1, /* attention's fused dot: a = XQKV [m, 3n] with
+                            [Q heads | K heads | V heads] 128-column head tiles, c = XDot
+                            [m, n]; XDot = Softmax(Q*V)*K per head and row (column-tile
+                            local, dropout p = 0); b unused. Tile = rows x tile_n columns
+                            (tile_n / 128 heads).                                         */
+  TS_STAGE_CONV2D = 2    /* 3x3 "same" convolution as implicit GeMM (PAPER.md:190-204,
+                            461-463): A gathered by an im2col TMA map, K order = input-
+                            channel tile (the producer's column tile) outer, filter tap,
+                            64-channel block inner, so Conv2DTileSync(9) waits once per
+                            producer column tile (policies.py:161-165)                   */
 } ts_stage_kind;
 
 typedef struct {

@@ -304,6 +304,26 @@ def swiglu_chain(x, w_gate, w_up, w_down, dtype="bf16"):
     return h, h @ w_down.astype(np.float32).T
 
 
+def conv3x3_nhwc(x, w):
+    """3x3, stride-1, padding-1 convolution as the implicit GeMM the device runs:
+    x NHWC [N, H, W, C], w KRSC [Co, 3, 3, C] -> NHWC [N, H, W, Co] (fp32). The K order of
+    the patch matrix is (tap r*3+s, channel), the KRSC weight row order."""
+    n, h, wd, c = x.shape
+    xp = np.zeros((n, h + 2, wd + 2, c), dtype=np.float32)
+    xp[:, 1:h + 1, 1:wd + 1] = x
+    cols = np.stack([xp[:, r:r + h, s_:s_ + wd] for r in range(3) for s_ in range(3)], axis=3)
+    a = cols.reshape(n * h * wd, 9 * c)
+    y = a @ w.reshape(w.shape[0], 9 * c).astype(np.float32).T
+    return y.reshape(n, h, wd, w.shape[0])
+
+
+def conv_chain(x, w1, w2, dtype="fp16"):
+    """A ResNet conv pair: H = ReLU(conv(X, W1)) rounded to the storage
+    dtype, Y = conv(H, W2) in fp32 (BatchNorm folded into the weights at inference)."""
+    h = round_to(np.maximum(conv3x3_nhwc(x.astype(np.float32), w1), 0.0), dtype)
+    return h, conv3x3_nhwc(h, w2)
+
+
 # ---- CPU executor of the paper's protocol --------------------------------------------------
 
 class _Sems:

@@ -7,7 +7,7 @@ sm_100a kernels execute. ``CuSync``/``CuStage`` are the paper's host API driving
 persistent tcgen05 chain kernel.
 """
 
-from .chains import AttentionChain, MlpChain, SwigluChain, interleave_gate_up, mlp
+from .chains import AttentionChain, ConvChain, MlpChain, SwigluChain, interleave_gate_up, mlp
 from .cusync import CuDep, CuStage, CuSync
 from .engine import (CostModel, Dependency, Event, Metrics, Mode, Scenario, SimOptions,
                      SimTrace, Stage, StageMetrics, avoid_wait_kernel, gated_producers,
@@ -33,5 +33,5 @@ __all__ = [
     "StridedRowMajor",
     "StridedSync", "SyncPolicy", "TileOrder", "TileSync", "WaitSpec", "check_policy",
     "consumer_wait", "is_sync", "order_tile", "post_target", "sem_count", "wait_steps",
-    "CuSync", "CuStage", "CuDep", "AttentionChain", "MlpChain", "SwigluChain", "interleave_gate_up", "mlp",
+    "CuSync", "CuStage", "CuDep", "AttentionChain", "ConvChain", "MlpChain", "SwigluChain", "interleave_gate_up", "mlp",
 ]

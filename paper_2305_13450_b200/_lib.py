@@ -21,9 +21,9 @@ TS_OK, TS_ERR_CONFIG, TS_ERR_VALUE, TS_ERR_TYPE, TS_ERR_CUDA, TS_ERR_DEADLOCK = 
 TS_POLICY_TILE, TS_POLICY_ROW, TS_POLICY_STRIDED, TS_POLICY_CONV2D = range(4)
 TS_ORDER_ROW_MAJOR, TS_ORDER_STRIDED_ROW_MAJOR, TS_ORDER_BANDED_COLUMN_MAJOR = range(3)
 TS_DTYPE_F16, TS_DTYPE_BF16 = range(2)
-TS_EPI_NONE, TS_EPI_GELU, TS_EPI_SWIGLU = range(3)
+TS_EPI_NONE, TS_EPI_GELU, TS_EPI_SWIGLU, TS_EPI_RELU = range(4)
 TS_MODE_STREAM, TS_MODE_FUSED = range(2)
-TS_STAGE_GEMM, TS_STAGE_ATTN_DOT = range(2)
+TS_STAGE_GEMM, TS_STAGE_ATTN_DOT, TS_STAGE_CONV2D = range(3)
 TS_FLAG_KEEP_SEMS, TS_FLAG_NO_REORDER, TS_FLAG_NO_WATCHDOG = 1, 2, 4
 
 TS_MAX_STAGES = 4
@@ -47,7 +47,9 @@ class StageDesc(ctypes.Structure):
         ("dtype", ctypes.c_int), ("epilogue", ctypes.c_int),
         ("order", ctypes.c_int), ("order_stride", ctypes.c_int),
         ("splits", ctypes.c_int), ("workspace", ctypes.c_void_p),
-        ("counters", ctypes.c_void_p), ("kind", ctypes.c_int), ("tile_n", ctypes.c_int),
+        ("counters", ctypes.c_void_p), ("kind", ctypes.c_int),
+        ("conv_n", ctypes.c_int), ("conv_h", ctypes.c_int), ("conv_w", ctypes.c_int),
+        ("tile_n", ctypes.c_int),
     ]
 
 

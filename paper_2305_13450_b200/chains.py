@@ -126,3 +126,33 @@ class AttentionChain:
     def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         self.cs.launch(stream)
         return self.y
+
+
+class ConvChain:
+    """A ResNet conv pair: ``H = ReLU(conv3x3(X, W1))``,
+    ``Y = conv3x3(H, W2)``, NHWC activations and KRSC weights (BatchNorm folded into the
+    weights at inference), synchronized with Conv2DTileSync(9): the
+    second convolution's k-step (input-channel tile, tap) waits for the producer tile that
+    wrote that channel tile of its rows (plus, untraced, the neighbouring row tiles its
+    3x3 window reaches)."""
+
+    def __init__(self, x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor,
+                 policy: SyncPolicy | None = None, mode: str = "fused", tile_n: int = 128,
+                 cta_group: int = 1, keep_sems: bool = False, num_ctas: int = 0,
+                 extra_flags: int = 0, prod_order: TileOrder = RowMajor(),
+                 cons_order: TileOrder = RowMajor(), act: str = "relu"):
+        from .policies import Conv2DTileSync
+        n, h, w, _ = x.shape
+        self.x, self.w1, self.w2 = x, w1, w2
+        self.h = torch.empty(n, h, w, w1.shape[0], dtype=x.dtype, device=x.device)
+        self.y = torch.empty(n, h, w, w2.shape[0], dtype=x.dtype, device=x.device)
+        self.cs = CuSync(tile_n=tile_n, mode=mode, keep_sems=keep_sems, num_ctas=num_ctas,
+                         cta_group=cta_group, extra_flags=extra_flags)
+        self.prod = self.cs.stage_conv(x, w1, self.h, epilogue=act, order=prod_order, id="conv1")
+        self.cons = self.cs.stage_conv(self.h, w2, self.y, order=cons_order, id="conv2")
+        self.dep = self.cs.dependency(policy or Conv2DTileSync(9), self.prod, self.cons,
+                                      operand="a")
+
+    def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        self.cs.launch(stream)
+        return self.y

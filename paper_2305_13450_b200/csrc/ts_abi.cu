@@ -73,6 +73,53 @@ int make_tmap(CUtensorMap* m, const void* ptr, int rows, int k, int ld, int dtyp
   return TS_OK;
 }
 
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const int*,
+                                    const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  });
+  return fn;
+}
+
+// im2col map over an NHWC activation tensor for a 3x3, stride-1, padding-1 convolution:
+// the pixel bounding box spans [-1, H-2] x [-1, W-2] (lower corner -pad, upper corner
+// pad - (R-1)), so output pixel (p, q) is box coordinate (p-1, q-1) and filter tap (r, s)
+// is the im2col offset; each load is `pixels` consecutive output pixels x 64 channels.
+int make_tmap_im2col(CUtensorMap* m, const void* ptr, int n, int h, int w, int c, int ldc_px,
+                     int dtype, int pixels) {
+  EncodeIm2colFn enc = encode_im2col_fn();
+  if (!enc) return fail(TS_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable (driver too old?)");
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w),
+                        static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
+  const cuuint64_t px = static_cast<cuuint64_t>(ldc_px) * 2;
+  cuuint64_t strides[3] = {px, px * w, px * w * h};
+  int lower[2] = {-1, -1};
+  int upper[2] = {-1, -1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, dtype == TS_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   4, const_cast<void*>(ptr), dims, strides, lower, upper, ts::kBK,
+                   static_cast<cuuint32_t>(pixels), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TS_ERR_CUDA, "cuTensorMapEncodeIm2col failed (%d) n=%d h=%d w=%d c=%d", (int)r, n,
+                h, w, c);
+  return TS_OK;
+}
+
 int sm_count() {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
@@ -155,7 +202,9 @@ int cta_group_of(const ts_chain_desc* d) {
 // 0 for the chain's tile width, -1 if its tile_n is not allowed.
 int stage_wide(const ts_stage_desc& st, int bn, int cg, int swap) {
   if (st.tile_n == 0 || st.tile_n == (swap ? 128 : bn)) return 0;
-  if (st.kind == TS_STAGE_GEMM && !swap && cg == 2 && bn == 256 && st.tile_n == 512) return 1;
+  if ((st.kind == TS_STAGE_GEMM || st.kind == TS_STAGE_CONV2D) && !swap && cg == 2 && bn == 256 &&
+      st.tile_n == 512)
+    return 1;
   return -1;
 }
 
@@ -242,10 +291,30 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       sp.last_arriver = 0;
       continue;
     }
-    if (st.kind != TS_STAGE_GEMM) return fail(TS_ERR_TYPE, "stage %d: unknown stage kind %d", s, st.kind);
-    sp.kind = ts::kStageGemm;
-    if (st.epilogue < TS_EPI_NONE || st.epilogue > TS_EPI_SWIGLU)
+    if (st.kind != TS_STAGE_GEMM && st.kind != TS_STAGE_CONV2D)
+      return fail(TS_ERR_TYPE, "stage %d: unknown stage kind %d", s, st.kind);
+    const bool conv = st.kind == TS_STAGE_CONV2D;
+    sp.kind = conv ? ts::kStageConv : ts::kStageGemm;
+    if (st.epilogue < TS_EPI_NONE || st.epilogue > TS_EPI_RELU)
       return fail(TS_ERR_TYPE, "stage %d: unknown epilogue %d", s, st.epilogue);
+    if (swap && st.epilogue == TS_EPI_RELU)
+      return fail(TS_ERR_CONFIG, "stage %d: the ReLU epilogue needs the normal tile layout", s);
+    if (conv) {
+      if (swap) return fail(TS_ERR_CONFIG, "stage %d: convolutions need the normal tile layout", s);
+      if (st.epilogue == TS_EPI_SWIGLU)
+        return fail(TS_ERR_CONFIG, "stage %d: no SwiGLU epilogue on a convolution", s);
+      if (st.conv_n < 1 || st.conv_h < 1 || st.conv_w < 1 ||
+          static_cast<long long>(st.conv_n) * st.conv_h * st.conv_w != st.m)
+        return fail(TS_ERR_VALUE, "stage %d: conv m=%d must equal n*h*w (%d*%d*%d)", s, st.m,
+                    st.conv_n, st.conv_h, st.conv_w);
+      if (st.k % 9 != 0 || (st.k / 9) % ts::kBK != 0)
+        return fail(TS_ERR_CONFIG, "stage %d: conv k=%d must be 9 x Cin with Cin a multiple of %d", s,
+                    st.k, ts::kBK);
+      if (st.lda < st.k / 9)
+        return fail(TS_ERR_VALUE, "stage %d: conv lda (pixel stride) %d < Cin %d", s, st.lda, st.k / 9);
+      if (st.conv_h > 32767 || st.conv_w > 32767)
+        return fail(TS_ERR_VALUE, "stage %d: image too large for the im2col map", s);
+    }
     if (swap && st.epilogue == TS_EPI_SWIGLU)
       return fail(TS_ERR_CONFIG, "stage %d: the SwiGLU epilogue needs the normal tile layout", s);
     if (st.m < 1 || st.n < 1 || st.k < 1)
@@ -267,7 +336,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     if (splits > 1 && (st.workspace == nullptr || st.counters == nullptr))
       return fail(TS_ERR_VALUE, "stage %d: split-K needs a workspace and counters", s);
     const int n_out = st.epilogue == TS_EPI_SWIGLU ? st.n / 2 : st.n;
-    if (st.lda < st.k || st.ldb < st.k || st.ldc < n_out || st.lda % 8 || st.ldb % 8 || st.ldc % 8)
+    if ((!conv && st.lda < st.k) || st.ldb < st.k || st.ldc < n_out || st.lda % 8 || st.ldb % 8 || st.ldc % 8)
       return fail(TS_ERR_VALUE, "stage %d: leading dimensions must cover the rows and be multiples of 8", s);
     if (!st.a || !st.b || !st.c) return fail(TS_ERR_VALUE, "stage %d: null operand pointer", s);
     if ((reinterpret_cast<uintptr_t>(st.a) | reinterpret_cast<uintptr_t>(st.b) |
@@ -281,6 +350,14 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.grid_x = (st.m + tile_m - 1) / tile_m;
     sp.grid_y = st.n / stage_tile_n;
     sp.wide = wide;
+    if (conv) {
+      if (splits > 1) return fail(TS_ERR_CONFIG, "stage %d: no split-K convolutions", s);
+      sp.conv_h = st.conv_h;
+      sp.conv_w = st.conv_w;
+      sp.conv_cin = st.k / 9;
+      sp.conv_subs = 1;  // K channel tile = 64 unless a producer's column tile sets it
+      sp.halo = (st.conv_w + 1 + tile_m - 1) / tile_m;
+    }
     sp.splits = splits;
     sp.ws = st.workspace;
     sp.cnt = st.counters;
@@ -307,7 +384,9 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     if (with_tmaps) {
       // activations: box rows = 128 per CTA (normal) or tile_n (swapped);
       // weights: box rows = tile_n / cta_group (normal) or 128 (swapped)
-      int r = make_tmap(&sp.tmap_a, st.a, st.m, st.k, st.lda, st.dtype, swap ? bn : 128);
+      int r = conv ? make_tmap_im2col(&sp.tmap_a, st.a, st.conv_n, st.conv_h, st.conv_w, st.k / 9,
+                                      st.lda, st.dtype, 128)
+                   : make_tmap(&sp.tmap_a, st.a, st.m, st.k, st.lda, st.dtype, swap ? bn : 128);
       if (r) return r;
       r = make_tmap(&sp.tmap_b, st.b, st.n, st.k, st.ldb, st.dtype, swap ? 128 : bn / cg);
       if (r) return r;
@@ -347,13 +426,24 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
         return fail(TS_ERR_CONFIG, "dependency %d: the dot stage must read its producer's [m, 3n] output", i);
       kb_per_kstep = 1;
       k_steps = 1;
+    } else if (cs.kind == ts::kStageConv) {
+      // a consumer k-step = (producer column tile, filter tap): Cin = producer columns
+      if (d->stages[dd.consumer].k != 9 * ps.grid_y * cols || cols % ts::kBK)
+        return fail(TS_ERR_CONFIG, "dependency %d: conv consumer k=%d must be 9 x producer output columns %d", i,
+                    d->stages[dd.consumer].k, ps.grid_y * cols);
+      if (dd.policy == ts::kConv2D && dd.param != 9)
+        return fail(TS_ERR_CONFIG, "dependency %d: a 3x3 conv consumer needs Conv2DTileSync(9), got kk=%d", i, dd.param);
+      if (dd.policy == ts::kStrided)
+        return fail(TS_ERR_CONFIG, "dependency %d: StridedSync cannot feed a convolution", i);
+      cs.conv_subs = cols / ts::kBK;
+      k_steps = cs.k_blocks / kb_per_kstep;
     } else {
       if (d->stages[dd.consumer].k != ps.grid_y * cols)
         return fail(TS_ERR_CONFIG, "dependency %d: consumer k=%d must equal producer output columns %d", i,
                     d->stages[dd.consumer].k, ps.grid_y * cols);
       k_steps = cs.k_blocks / kb_per_kstep;
     }
-    if (dd.policy == ts::kConv2D) {
+    if (dd.policy == ts::kConv2D && cs.kind != ts::kStageConv) {
       if (kb_per_kstep % dd.param != 0)
         return fail(TS_ERR_CONFIG, "dependency %d: kk=%d does not divide the %d K-blocks of a producer tile", i, dd.param, kb_per_kstep);
       kb_per_kstep /= dd.param;

@@ -48,6 +48,7 @@ constexpr int kCommitRing = 16;  // > commit groups in flight
 constexpr uint64_t kWatchdogNs = 4000000000ull;
 constexpr int kStageGemm = 0;  // C = epi(A x B^T) on tcgen05
 constexpr int kStageDot = 1;   // attention's fused softmax-dot over QKV column tiles
+constexpr int kStageConv = 2;  // 3x3 "same" Conv2D as implicit GeMM (im2col TMA A operand)
 
 // K-blocks per tcgen05.commit (flags bits 17-18: 1 -> 1, 2 -> 2, 3 -> 4; 0 -> default 2).
 __host__ __device__ __forceinline__ int commit_group(int flags) {
@@ -82,6 +83,13 @@ struct StageParams {
   int dot_dep;       // producer side: dependency index, or -1
   int last_arriver;  // dot side: 1 when its tiles run on the last-arriving producer
   int wide;          // 1: double-width pair tile (2 x BN output columns, Cfg::kChunked)
+  // kStageConv: NHWC input [conv_n, conv_h, conv_w, conv_cin] (tmap_a is an im2col map),
+  // KRSC weights [n, 3, 3, conv_cin] (tmap_b over [n, 9 conv_cin]). K-block order:
+  // input-channel tile (conv_subs x 64 channels) outer, filter tap, 64-channel sub-block
+  // inner — a consumer k-step is one (producer column tile, tap) pair, as
+  // Conv2DTileSync's k // kk map requires (policies.py:161-165). `halo` = producer row
+  // tiles on each side a consumer tile's 3x3 window reaches (extra, untraced waits).
+  int conv_h, conv_w, conv_cin, conv_subs, halo;
 };
 
 struct DepParams {
@@ -193,6 +201,8 @@ template <>
 struct AbFormat<__nv_bfloat16> {
   static constexpr uint32_t value = 1;
 };
+
+__device__ __forceinline__ float relu(float x) { return fmaxf(x, 0.f); }
 
 // GeLU in GPT-3's tanh form (GPT-2/3 "gelu_new"), with the hardware
 // tanh: 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))).
@@ -498,8 +508,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         // stage.wait() for reference k-step `ks` (policies.py:145-166)
         auto wait_kstep = [&](int ks) {
           const DepParams& dp = p.dep[d];
-          Wait w = consumer_wait(dp.policy, dp.param, t.tx, t.ty, ks,
-                                 Grid3{dp.pgx, dp.pgy, dp.pgz}, dp.pgz);
+          const Grid3 pg{dp.pgx, dp.pgy, dp.pgz};
+          Wait w = consumer_wait(dp.policy, dp.param, t.tx, t.ty, ks, pg, dp.pgz);
           if (w.sem < 0) return;
           if (leader)
             trace_event(p, ptx::global_timer(), 1, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
@@ -508,8 +518,25 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           if (leader)
             trace_event(p, ptx::global_timer(), 2, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
                         t.ty, t.tz);
+          // Halo (extension, untraced): a 3x3 window of output rows [m0, m0 + tile_m)
+          // reads input pixels up to W + 1 rows away, i.e. the same k-step's producer
+          // tiles of neighbouring row tiles. The reference map names only row tx.
+          for (int dx = -st.halo; dx <= st.halo; ++dx) {
+            const int x = t.tx + dx;
+            if (dx == 0 || x < 0 || x >= dp.pgx) continue;
+            Wait h = consumer_wait(dp.policy, dp.param, x, t.ty, ks, pg, dp.pgz);
+            if (h.sem >= 0) sem_wait(p, dp.sem + h.sem, h.expected);
+          }
           ptx::fence_proxy_async_global();
         };
+        // conv: the first output pixel of this CTA's rows, as NHW coordinates
+        const bool conv = st.kind == kStageConv;
+        int cq = 0, cp = 0, cn = 0;
+        if (conv) {
+          cq = act_row % st.conv_w;
+          cp = (act_row / st.conv_w) % st.conv_h;
+          cn = act_row / (st.conv_w * st.conv_h);
+        }
         const bool waits = d >= 0 && !no_wait;
         const int kbpk = waits ? p.dep[d].kb_per_kstep : 1;
         // K-loop rotation. At small batch every tile reads the same few activation lines
@@ -519,7 +546,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         // weight block (same ty) stay in lockstep for L2 reuse. Allowed when the policy
         // has no k-step ordering to respect (no dependency, or a single wait at k-step 0).
         const bool ordered = waits && !(p.dep[d].policy == kRow || p.dep[d].policy == kStrided);
-        const int rot = (ordered || (p.flags >> 14) & 1) ? 0 : (t.ty * 37 + 5) % k_per;
+        const int rot = (ordered || conv || (p.flags >> 14) & 1) ? 0 : (t.ty * 37 + 5) % k_per;
         if (waits && rot != 0) {
           // every wait of the slice (only k-step 0 waits for Row/Strided) before any load
           for (int ks = 0; ks * kbpk < st.k_blocks; ++ks) wait_kstep(ks);
@@ -567,19 +594,39 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             act_dst = SW ? sB + e0 * C::kBBytes : sA + e0 * C::kABytes;
             w_dst = SW ? sA + e0 * C::kABytes : sB + e0 * C::kBBytes;
           }
+          // weight K coordinate; conv: K-block kb = (channel tile, tap, sub-block)
+          int wk = kb * kBK, c0 = 0, tap = 0;
+          if (conv) {
+            const int per_tile = 9 * st.conv_subs;
+            const int rem = kb % per_tile;
+            tap = rem / st.conv_subs;
+            c0 = ((kb / per_tile) * st.conv_subs + rem % st.conv_subs) * kBK;
+            wk = tap * st.conv_cin + c0;  // KRSC: [tap][cin] inside a weight row
+          }
           auto load_b = [&]() {
             if constexpr (CG == 2) {
-              ptx::tma_load_2d_pair(w_dst, &st.tmap_b, fbc, kb * kBK, w_row, pol_b);
+              ptx::tma_load_2d_pair(w_dst, &st.tmap_b, fbc, wk, w_row, pol_b);
               if (C::kChunked && wide)
-                ptx::tma_load_2d_pair(smem + e2 * C::kChunkBytes, &st.tmap_b, fbc, kb * kBK,
+                ptx::tma_load_2d_pair(smem + e2 * C::kChunkBytes, &st.tmap_b, fbc, wk,
                                       w_row + BN, pol_b);
             } else {
-              ptx::tma_load_2d(w_dst, &st.tmap_b, fb, kb * kBK, w_row, pol_b);
+              ptx::tma_load_2d(w_dst, &st.tmap_b, fb, wk, w_row, pol_b);
             }
           };
           if (reorder) load_b();
           if (waits && rot == 0 && kb % kbpk == 0) wait_kstep(kb / kbpk);
           if (skip_act) {
+          } else if (conv) {
+            // im2col box: 128 consecutive output pixels' inputs at filter tap (r, s), 64
+            // channels from c0; the map's bounding box starts at (-1, -1), so pixel (p, q)
+            // sits at box coordinate (p - 1, q - 1) and the tap adds (r, s); outside the
+            // image the TMA fills zeros (the 3x3 "same" padding).
+            const uint16_t r = static_cast<uint16_t>(tap / 3), s = static_cast<uint16_t>(tap % 3);
+            if constexpr (CG == 2) {
+              ptx::tma_load_im2col_pair(act_dst, &st.tmap_a, fbc, c0, cq - 1, cp - 1, cn, s, r, pol_a);
+            } else {
+              ptx::tma_load_im2col(act_dst, &st.tmap_a, fb, c0, cq - 1, cp - 1, cn, s, r, pol_a);
+            }
           } else if constexpr (CG == 2) {
             ptx::tma_load_2d_pair(act_dst, &st.tmap_a, fbc, kb * kBK, act_row, pol_a);
           } else {
@@ -935,6 +982,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       } else {
         T* out = crow + t.ty * acc_cols;
         const bool gl = st.epilogue == TS_EPI_GELU;
+        const bool rl = st.epilogue == TS_EPI_RELU;
         // Column group eg stores accumulator columns [eg * span, (eg + 1) * span); slot
         // by slot, so a slot is handed back to the MMA warp as soon as every group is
         // done with it (a group arrives on a slot it does not read right away).
@@ -954,6 +1002,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
               if (gl) {
                 v0 = gelu(v0);
                 v1 = gelu(v1);
+              } else if (rl) {
+                v0 = relu(v0);
+                v1 = relu(v1);
               }
               pk[q] = pack2<T>(v0, v1);
             }

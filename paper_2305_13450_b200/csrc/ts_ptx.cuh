@@ -160,6 +160,32 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       : "memory");
 }
 
+// 4-D im2col load (NHWC): `pixelsPerColumn` consecutive pixels of the map's bounding box
+// from (w, h, n), channels [c, c + channelsPerPixel), each pixel shifted by the filter
+// tap offsets (ow, oh); out-of-image pixels read as zero.
+__device__ __forceinline__ void tma_load_im2col(void* dst, const CUtensorMap* m, uint64_t* bar,
+                                                int c, int w, int h, int n, uint16_t ow,
+                                                uint16_t oh, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8}, %9;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
+      "h"(ow), "h"(oh), "l"(cache_hint)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_im2col_pair(void* dst, const CUtensorMap* m,
+                                                     uint32_t bar_cluster, int c, int w, int h,
+                                                     int n, uint16_t ow, uint16_t oh,
+                                                     uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx"
+      "::bytes.L2::cache_hint [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8}, %9;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c), "r"(w), "r"(h), "r"(n),
+      "h"(ow), "h"(oh), "l"(cache_hint)
+      : "memory");
+}
+
 // L2 cache-policy descriptors (createpolicy) for streaming weights vs reused activations.
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;

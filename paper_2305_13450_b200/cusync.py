@@ -37,7 +37,8 @@ from .policies import (Conv2DTileSync, RowMajor, SyncPolicy, TileOrder, order_co
 
 BM = 128
 BK = 64
-_EPI = {"none": _lib.TS_EPI_NONE, "gelu": _lib.TS_EPI_GELU, "swiglu": _lib.TS_EPI_SWIGLU}
+_EPI = {"none": _lib.TS_EPI_NONE, "gelu": _lib.TS_EPI_GELU, "swiglu": _lib.TS_EPI_SWIGLU,
+        "relu": _lib.TS_EPI_RELU}
 _DT = {torch.float16: _lib.TS_DTYPE_F16, torch.bfloat16: _lib.TS_DTYPE_BF16}
 _KINDS = ("scheduled", "wait_begin", "wait_end", "post", "finished")
 # Replay order for events sharing a timestamp: posts before the waits they justify
@@ -60,7 +61,8 @@ class CuStage:
     splits: int = 1
     ws: torch.Tensor | None = None
     cnt: torch.Tensor | None = None
-    kind: str = "gemm"  # "gemm" or "dot" (attention's fused softmax-dot)
+    kind: str = "gemm"  # "gemm", "dot" (attention's fused softmax-dot) or "conv"
+    conv: tuple | None = None  # (N, H, W) of a 3x3 "same" convolution stage
     tile_n: int = 0     # 0 = the chain's tile_n; 512 = double-width CTA-pair tile
 
     @property
@@ -74,7 +76,8 @@ class CuStage:
 
     @property
     def k(self) -> int:
-        return self.a.shape[1]
+        """Reduction length (9 x Cin for a convolution: KRSC weight row length)."""
+        return self.b.shape[1] if self.kind == "conv" else self.a.shape[1]
 
     @property
     def width(self) -> int:
@@ -212,6 +215,39 @@ class CuSync:
         self._desc = None
         return st
 
+    def stage_conv(self, x: torch.Tensor, w: torch.Tensor, out: torch.Tensor,
+                   epilogue: str = "none", order: TileOrder = RowMajor(), id: str | None = None,
+                   tile_n: int = 0) -> CuStage:
+        """A 3x3, stride-1, padding-1 Conv2D as an implicit GeMM (the paper's ResNet conv
+        pairs, PAPER.md:186-204): ``x`` NHWC [N, H, W, Cin], ``w`` KRSC [Cout, 3, 3, Cin],
+        ``out`` NHWC [N, H, W, Cout]. Output rows are the N*H*W pixels, columns the output
+        channels; the A operand is gathered by an im2col TMA map (zero padding at the
+        image border). Feed it from another stage with ``Conv2DTileSync(9)``."""
+        if len(self.stages) >= _lib.TS_MAX_STAGES:
+            raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
+        if epilogue not in ("none", "relu", "gelu"):
+            raise ConfigError(f"unsupported conv epilogue {epilogue!r}")
+        if x.dim() != 4 or out.dim() != 4 or w.dim() != 4 or tuple(w.shape[1:3]) != (3, 3):
+            raise ValueError("conv needs x [N,H,W,Cin], w [Cout,3,3,Cin], out [N,H,W,Cout]")
+        for t, name in ((x, "x"), (w, "w"), (out, "out")):
+            if not t.is_contiguous() or t.dtype not in _DT or not t.is_cuda:
+                raise ValueError(f"{name} must be a contiguous fp16/bf16 CUDA tensor")
+        n, h, wd, cin = x.shape
+        if w.shape[3] != cin or tuple(out.shape) != (n, h, wd, w.shape[0]):
+            raise ValueError(f"shape mismatch: x {tuple(x.shape)} w {tuple(w.shape)} "
+                             f"out {tuple(out.shape)}")
+        if tile_n not in (0, self.tile_n) and not (
+                tile_n == 512 and self.tile_n == 256 and self.cta_group == 2 and not self.swap_ab):
+            raise ConfigError(f"stage tile_n {tile_n} unsupported")
+        st = CuStage(self, len(self.stages), id or f"conv{len(self.stages) + 1}",
+                     x.view(n * h * wd, cin), w.reshape(w.shape[0], 9 * cin),
+                     out.view(n * h * wd, w.shape[0]), epilogue, order, kind="conv",
+                     conv=(n, h, wd), tile_n=tile_n)
+        self.stages.append(st)
+        self.device = x.device
+        self._desc = None
+        return st
+
     def dependency(self, policy: SyncPolicy, producer: CuStage, consumer: CuStage,
                    operand: str = "a") -> CuDep:
         """cs.dependency<Policy>(prod, cons, operand) — allocates the semaphore array."""
@@ -237,8 +273,8 @@ class CuSync:
                 k_steps = max(1, st.k // st.out_tile_cols)
             else:
                 k_steps = st.k // d.producer.out_tile_cols
-                if isinstance(d.policy, Conv2DTileSync):
-                    k_steps *= d.policy.kk
+                if isinstance(d.policy, Conv2DTileSync) and st.kind != "conv":
+                    k_steps *= d.policy.kk  # a GeMM consumer splits producer tiles kk-fold
             operands = ("qkv",) if st.kind == "dot" else ("a", "b")
             stages.append(Stage(id=st.id, grid=st.grid, occupancy=1, k_steps=k_steps,
                                 order=st.order, operands=operands))
@@ -262,7 +298,10 @@ class CuSync:
             sd.epilogue = _EPI[st.epilogue]
             sd.order, sd.order_stride = order_code(st.order)
             sd.splits = st.splits
-            sd.kind = _lib.TS_STAGE_ATTN_DOT if st.kind == "dot" else _lib.TS_STAGE_GEMM
+            sd.kind = {"dot": _lib.TS_STAGE_ATTN_DOT, "conv": _lib.TS_STAGE_CONV2D}.get(
+                st.kind, _lib.TS_STAGE_GEMM)
+            if st.conv is not None:
+                sd.conv_n, sd.conv_h, sd.conv_w = st.conv
             sd.tile_n = st.tile_n
             sd.workspace = st.ws.data_ptr() if st.ws is not None else None
             sd.counters = st.cnt.data_ptr() if st.cnt is not None else None

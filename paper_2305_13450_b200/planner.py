@@ -51,9 +51,13 @@ def candidates(m: int, mode: str):
                                 prod_splits=z1, cons_splits=z2))
     for cg, tn in ((2, 256), (1, 256), (2, 128), (1, 128)):
         gx = -(-m // (128 * cg))
-        orders = [RowMajor()] + ([BandedColumnMajor(gx)] if gx > 1 else [])
-        for pol, co in itertools.product(pols, orders):
-            out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=cg, cons_order=co))
+        orders = [RowMajor()] + ([BandedColumnMajor(min(gx, 4))] if gx > 1 else [])
+        # per-stage widths: CTA-pair 256-wide chains may give either stage double-width
+        # (256 x 512) tiles — fewer operand bytes per MAC, coarser wave quantization
+        widths = [(0, 0), (0, 512), (512, 512), (512, 0)] if (cg, tn) == (2, 256) else [(0, 0)]
+        for pol, co, (pw, cw) in itertools.product(pols, orders, widths):
+            out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=cg, cons_order=co,
+                            prod_tile_n=pw, cons_tile_n=cw))
     return out
 
 
@@ -62,7 +66,10 @@ def describe(kw) -> dict:
     swap = kw.get("swap_ab", False)
     tile = f"128x{kw['tile_n']}" if not swap else f"{kw['tile_n']}x128 (swapped)"
     if not swap:
-        tile = f"{128 * kw['cta_group']}x{kw['tile_n']}"
+        m = 128 * kw["cta_group"]
+        pw = kw.get("prod_tile_n") or kw["tile_n"]
+        cw = kw.get("cons_tile_n") or kw["tile_n"]
+        tile = f"{m}x{pw}" if pw == cw else f"{m}x{pw}/{m}x{cw}"
     return {"mode": kw["mode"], "policy": type(kw["policy"]).__name__, "tile": tile,
             "cta_group": kw["cta_group"], "swap_ab": swap,
             "splits": [kw.get("prod_splits", 1), kw.get("cons_splits", 1)],
@@ -150,3 +157,56 @@ def wave_table(m: int, n1: int, n2: int, tile_m: int, tile_n: int, sms: int = 14
     fine = waves(t1 + t2, g, 1).ceil
     return {"tiles": (t1, t2), "stream_waves": stream, "fine_waves": fine,
             "bound": stream / fine}
+
+
+RESNET38_LAYERS = ((56, 64), (28, 128), (14, 256), (7, 512))
+
+
+def conv_candidates(c: int, mode: str):
+    """Tile configurations for a conv pair with `c` channels (output channels = tile
+    columns: a tile no wider than the layer)."""
+    out = []
+    for cg, tn in ((1, 64), (1, 128), (2, 128), (1, 256), (2, 256)):
+        if tn > c:
+            continue
+        out.append(dict(mode=mode, tile_n=tn, cta_group=cg))
+    return out
+
+
+def sweep_conv(batches=(1, 8, 32, 128, 256), layers=RESNET38_LAYERS, device=None,
+               dtype=torch.float16):
+    """ResNet-38 conv pairs (3x3, same padding): best fused (Conv2DTileSync(9)) vs best
+    stream-synchronized launch of the same kernels vs cuDNN (channels-last conv2d)."""
+    from .chains import ConvChain
+    torch.manual_seed(11)
+    rows = []
+    for hw, c in layers:
+        w1 = (torch.randn(c, 3, 3, c, device=device) / (9 * c) ** 0.5).to(dtype)
+        w2 = (torch.randn(c, 3, 3, c, device=device) / (9 * c) ** 0.5).to(dtype)
+        wt1 = w1.permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last)
+        wt2 = w2.permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last)
+        for b in batches:
+            x = torch.randn(b, hw, hw, c, device=device).to(dtype)
+            best = {}
+            for mode in ("fused", "stream"):
+                for kw in conv_candidates(c, mode):
+                    ch = ConvChain(x, w1, w2, **kw)
+                    us = _time(ch, iters=20)
+                    if ch.cs.watchdog_fired():
+                        continue
+                    if mode not in best or us < best[mode][0]:
+                        best[mode] = (us, kw)
+            xt = x.permute(0, 3, 1, 2)  # NCHW view of NHWC memory = channels_last
+
+            def cudnn():
+                h = torch.relu(torch.nn.functional.conv2d(xt, wt1, padding=1))
+                return torch.nn.functional.conv2d(h, wt2, padding=1)
+            cu = _time(cudnn, iters=20)
+            flops = 2 * 2 * b * hw * hw * c * 9 * c
+            fu, su = best["fused"][0], best["stream"][0]
+            rows.append({"layer": f"{hw}x{hw}x{c}", "batch": b, "fused_us": fu, "stream_us": su,
+                         "cudnn_us": cu, "speedup_vs_stream": su / fu, "speedup_vs_cudnn": cu / fu,
+                         "fused_tflops": flops / fu / 1e6,
+                         "fused": {k: v for k, v in best["fused"][1].items() if k != "mode"},
+                         "stream": {k: v for k, v in best["stream"][1].items() if k != "mode"}})
+    return rows

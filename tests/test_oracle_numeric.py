@@ -56,3 +56,26 @@ def test_cpu_protocol_executor(policy):
               {"id": "c", "grid": (3, 3, 1), "k_steps": 4, "order": (O.ROW_MAJOR, 1)}]
     deps = [{"producer": "p", "consumer": "c", "operand": "a", "policy": policy}]
     assert sems == O.final_semaphores(stages, deps)["p->c/a"]
+
+
+def test_conv3x3_matches_torch_float64():
+    """The implicit-GeMM conv restatement against torch's direct conv2d in float64."""
+    import torch
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((2, 7, 9, 16)).astype(np.float32)
+    w = rng.standard_normal((24, 3, 3, 16)).astype(np.float32)
+    ref = torch.nn.functional.conv2d(torch.from_numpy(x).double().permute(0, 3, 1, 2),
+                                     torch.from_numpy(w).double().permute(0, 3, 1, 2),
+                                     padding=1).permute(0, 2, 3, 1).numpy()
+    got = O.conv3x3_nhwc(x, w)
+    assert np.abs(got - ref).max() < 1e-3 * np.abs(ref).max()
+
+
+def test_conv_chain_relu_and_rounding():
+    rng = np.random.default_rng(4)
+    x = O.round_to(rng.standard_normal((1, 5, 6, 8)).astype(np.float32), "fp16")
+    w1 = O.round_to(rng.standard_normal((8, 3, 3, 8)).astype(np.float32) / 8, "fp16")
+    w2 = O.round_to(rng.standard_normal((4, 3, 3, 8)).astype(np.float32) / 8, "fp16")
+    h, y = O.conv_chain(x, w1, w2, "fp16")
+    assert (h >= 0).all() and np.array_equal(h, O.round_to(h, "fp16"))
+    assert np.allclose(y, O.conv3x3_nhwc(h, w2))
