@@ -127,20 +127,25 @@ typedef struct {
   int epilogue;  /* ts_epilogue */
   int order;     /* ts_order_kind */
   int order_stride;
-  int splits;        /* split-K slices (the reference's z extent); 0/1 = none.
-                        > 1 needs swap_ab, a workspace and counters */
-  float* workspace;  /* splits > 1: device fp32[tiles * splits * tile_n * 128]         */
-  int* counters;     /* splits > 1: device int32[tiles], zero on entry (kept zero)     */
+  int splits;        /* split-K slices (the reference's z extent); 0/1 = none. Each
+                        slice posts once; the last to arrive sums the fp32 partials and
+                        applies the epilogue (GeMM stages, not SwiGLU) */
+  float* workspace;  /* splits > 1: device fp32[tiles * splits * tile_m * tile_cols]
+                        (tile_m = rows of a tile: 128 x cta_group, or tile_n swapped;
+                        tile_cols = accumulator columns: the stage's tile width, or 128
+                        swapped)                                                       */
+  int* counters;     /* splits > 1: device int32[tiles * cta_group], zero on entry
+                        (kept zero)                                                    */
   int kind;          /* ts_stage_kind */
   int conv_n, conv_h, conv_w; /* TS_STAGE_CONV2D: image batch, height, width (3x3 kernel,
                         stride 1, padding 1: output H x W = input H x W); m = n*h*w,
                         k = 9 * Cin, a = NHWC input (lda = Cin), b = KRSC weights
                         [n][3][3][Cin] (ldb >= 9 Cin), c = NHWC output [m, n]        */
-  int tile_n;        /* this stage's tile width: 0 = the chain's tile_n; 512 = a
-                        double-width CTA-pair tile (256 x 512 outputs: one A box feeds
-                        two N = 256 MMAs, 25 % fewer operand bytes per MAC), allowed
-                        for GeMM stages of cta_group 2, tile_n 256 chains that do not
-                        feed a dot stage */
+  int tile_n;        /* this stage's tile width: 0 = the chain's tile_n; 384 or 512 = a
+                        CTA-pair tile of two MMAs per K-block (256 x 384: 2 x N=192;
+                        256 x 512: 2 x N=256) sharing one A box — fewer operand bytes
+                        per MAC than 256 x 256. GeMM and conv stages of cta_group 2,
+                        tile_n 256 chains that do not feed a dot stage */
 } ts_stage_desc;
 
 typedef enum {

@@ -198,21 +198,27 @@ int cta_group_of(const ts_chain_desc* d) {
   return d->cta_group == 0 ? 2 : d->cta_group;
 }
 
-// 1 if GeMM stage `st` uses double-width CTA-pair tiles (ts_stage_desc.tile_n = 512),
-// 0 for the chain's tile width, -1 if its tile_n is not allowed.
+// 1 if GeMM/conv stage `st` uses two MMAs per K-block step (CTA-pair tiles of
+// ts_stage_desc.tile_n = 512: 2 x 256 columns, or 384: 2 x 192 columns), 0 for the
+// chain's tile width, -1 if its tile_n is not allowed.
 int stage_wide(const ts_stage_desc& st, int bn, int cg, int swap) {
   if (st.tile_n == 0 || st.tile_n == (swap ? 128 : bn)) return 0;
   if ((st.kind == TS_STAGE_GEMM || st.kind == TS_STAGE_CONV2D) && !swap && cg == 2 && bn == 256 &&
-      st.tile_n == 512)
+      (st.tile_n == 512 || st.tile_n == 384))
     return 1;
   return -1;
+}
+
+// Columns per MMA (and per TMEM accumulator slot) of stage `st`.
+int stage_half_n(const ts_stage_desc& st, int bn, int cg, int swap) {
+  return stage_wide(st, bn, cg, swap) > 0 ? st.tile_n / 2 : bn;
 }
 
 // Output columns one tile of stage `st` writes (the producer "column tile" width that a
 // consumer k-step covers).
 int out_tile_cols(const ts_stage_desc& st, int bn, int cg, int swap) {
   if (swap) return 128;
-  const int w = stage_wide(st, bn, cg, swap) > 0 ? 2 * bn : bn;
+  const int w = stage_wide(st, bn, cg, swap) > 0 ? st.tile_n : bn;
   return st.epilogue == TS_EPI_SWIGLU ? w / 2 : w;
 }
 
@@ -321,9 +327,10 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       return fail(TS_ERR_VALUE, "stage %d: m, n, k must be >= 1", s);
     const int wide = stage_wide(st, bn, cg, swap);
     if (wide < 0)
-      return fail(TS_ERR_CONFIG, "stage %d: tile_n %d unsupported (0, %d, or 512 with cta_group 2 "
-                  "and chain tile_n 256)", s, st.tile_n, tile_n);
-    const int stage_tile_n = tile_n << wide;
+      return fail(TS_ERR_CONFIG, "stage %d: tile_n %d unsupported (0, %d, or 384 / 512 with "
+                  "cta_group 2 and chain tile_n 256)", s, st.tile_n, tile_n);
+    const int half_n = stage_half_n(st, bn, cg, swap);
+    const int stage_tile_n = swap ? tile_n : half_n << wide;
     if (st.n % stage_tile_n != 0)
       return fail(TS_ERR_CONFIG, "stage %d: n=%d is not a multiple of the tile width %d", s, st.n,
                   stage_tile_n);
@@ -331,8 +338,8 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     if (st.k % (ts::kBK * splits) != 0)
       return fail(TS_ERR_CONFIG, "stage %d: k=%d is not a multiple of %d x %d split(s)", s, st.k,
                   ts::kBK, splits);
-    if (splits > 1 && !swap)
-      return fail(TS_ERR_CONFIG, "stage %d: split-K needs swap_ab tiles", s);
+    if (splits > 1 && !swap && st.epilogue == TS_EPI_SWIGLU)
+      return fail(TS_ERR_CONFIG, "stage %d: split-K has no SwiGLU epilogue", s);
     if (splits > 1 && (st.workspace == nullptr || st.counters == nullptr))
       return fail(TS_ERR_VALUE, "stage %d: split-K needs a workspace and counters", s);
     const int n_out = st.epilogue == TS_EPI_SWIGLU ? st.n / 2 : st.n;
@@ -350,6 +357,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.grid_x = (st.m + tile_m - 1) / tile_m;
     sp.grid_y = st.n / stage_tile_n;
     sp.wide = wide;
+    sp.half_n = half_n;
     if (conv) {
       if (splits > 1) return fail(TS_ERR_CONFIG, "stage %d: no split-K convolutions", s);
       sp.conv_h = st.conv_h;
@@ -388,7 +396,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
                                       st.lda, st.dtype, 128)
                    : make_tmap(&sp.tmap_a, st.a, st.m, st.k, st.lda, st.dtype, swap ? bn : 128);
       if (r) return r;
-      r = make_tmap(&sp.tmap_b, st.b, st.n, st.k, st.ldb, st.dtype, swap ? 128 : bn / cg);
+      r = make_tmap(&sp.tmap_b, st.b, st.n, st.k, st.ldb, st.dtype, swap ? 128 : half_n / cg);
       if (r) return r;
     }
   }

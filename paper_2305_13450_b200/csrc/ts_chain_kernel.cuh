@@ -82,7 +82,8 @@ struct StageParams {
   // right away. `dot_dep` is this (producer) stage's dependency into such a dot stage.
   int dot_dep;       // producer side: dependency index, or -1
   int last_arriver;  // dot side: 1 when its tiles run on the last-arriving producer
-  int wide;          // 1: double-width pair tile (2 x BN output columns, Cfg::kChunked)
+  int wide;          // 1: two MMAs per K-block step (Cfg::kChunked): 2 x half_n columns
+  int half_n;        // columns per MMA / accumulator slot: BN, or 192 (256 x 384 tiles)
   // kStageConv: NHWC input [conv_n, conv_h, conv_w, conv_cin] (tmap_a is an im2col map),
   // KRSC weights [n, 3, 3, conv_cin] (tmap_b over [n, 9 conv_cin]). K-block order:
   // input-channel tile (conv_subs x 64 channels) outer, filter tap, 64-channel sub-block
@@ -494,7 +495,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         // a double-width tile's second B box (output columns [BN, 2 BN) of the pair
         // tile) starts BN weight rows further; each CTA holds its 128-row half of both
         const int wide = C::kChunked ? st.wide : 0;
-        const int w_row = SW ? t.ty * 128 : t.ty * (BN << wide) + static_cast<int>(rank) * C::kBRows;
+        const int hn = C::kChunked ? st.half_n : BN;  // columns per MMA
+        const int w_row = SW ? t.ty * 128 : t.ty * (hn << wide) + static_cast<int>(rank) * (hn / CG);
         const int d = st.in_dep;
         const int bh = b_hint ? b_hint : (st.grid_x == 1 ? 1 : 2);
         const uint64_t pol_b = bh == 1 ? pol_first : (bh == 2 ? pol_normal : pol_last);
@@ -580,7 +582,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           const uint32_t fbc = CG == 2 ? ptx::mapa(fb, 0) : 0;  // the leader CTA's barrier
           if (leader) {
             const int nc = 2 + wide;
-            const int bytes = C::kChunked ? C::kChunkBytes * (skip_act ? nc - 1 : nc)
+            // chunked: A box (128 rows) + 1-2 B boxes of hn / 2 rows, 128 B each
+            const int bytes = C::kChunked ? (skip_act ? 0 : C::kChunkBytes) + (nc - 1) * (hn / 2) * 128
                                           : (skip_act ? (SW ? C::kABytes : C::kBBytes)
                                                       : C::kStageBytes);
             ptx::mbar_arrive_expect_tx(fb, CG * bytes);
@@ -608,7 +611,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
               ptx::tma_load_2d_pair(w_dst, &st.tmap_b, fbc, wk, w_row, pol_b);
               if (C::kChunked && wide)
                 ptx::tma_load_2d_pair(smem + e2 * C::kChunkBytes, &st.tmap_b, fbc, wk,
-                                      w_row + BN, pol_b);
+                                      w_row + hn, pol_b);
             } else {
               ptx::tma_load_2d(w_dst, &st.tmap_b, fb, wk, w_row, pol_b);
             }
@@ -663,6 +666,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         if (sp.kind == kStageDot) continue;  // no MMA, no accumulator buffer
         const int kblocks = sp.k_blocks / sp.splits;
         const int wide = C::kChunked ? sp.wide : 0;
+        // instruction descriptor: N = the stage's columns per MMA (chunked stages)
+        const uint32_t idesc = C::kChunked ? ptx::idesc_f16(128 * CG, sp.half_n, AbFormat<T>::value)
+                                           : kIdesc;
         // TMEM reuse only (for pairs, tcgen05 fences order the peer's loads)
         for (int j = 0; j <= wide; ++j)
           ptx::mbar_wait(&tmem_empty[(u + j) & 1], (((u + j) >> 1) & 1) ^ 1);
@@ -697,8 +703,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
               const uint64_t ad = desc(ea);
               const int eb2 = eb + 1 == R ? C::kAChunks : eb + 1;
               if (!no_mma) {
-                ptx::umma_f16_kblock<CG>(d_tmem, ad, desc(eb), kIdesc, kb != 0);
-                if (wide) ptx::umma_f16_kblock<CG>(d_tmem2, ad, desc(eb2), kIdesc, kb != 0);
+                ptx::umma_f16_kblock<CG>(d_tmem, ad, desc(eb), idesc, kb != 0);
+                if (wide) ptx::umma_f16_kblock<CG>(d_tmem2, ad, desc(eb2), idesc, kb != 0);
               }
             } else {
               const int rs = ea;
@@ -832,6 +838,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       }
       const uint32_t acc = local & 1;
       const int wide = C::kChunked ? st.wide : 0;
+      const int hn = C::kChunked ? st.half_n : BN;  // accumulator columns per slot
       for (int j = 0; j <= wide; ++j)  // arrived by the MMA commits
         ptx::mbar_wait(&tmem_full[(u + j) & 1], ((u + j) >> 1) & 1);
       ptx::tc_fence_after();
@@ -841,7 +848,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       const uint32_t t_lane = lane_base + (u & 1) * C::kAccCols;
       // accumulator column x of this tile (a double-width tile spans both slots)
       auto tcol = [&](int x) -> uint32_t {
-        return lane_base + ((u + x / BN) & 1) * C::kAccCols + (x % BN);
+        return lane_base + ((u + x / hn) & 1) * C::kAccCols + (x % hn);
       };
       auto release_slot = [&](int j) {
         ptx::tc_fence_before();
@@ -952,11 +959,89 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       const int row = t.tx * C::kTileM + static_cast<int>(rank) * 128 + ew * 32 + lane;
       const bool row_ok = row < st.m;
       T* crow = reinterpret_cast<T*>(st.c) + static_cast<size_t>(row) * st.ldc;
-      const int acc_cols = BN << wide;  // accumulator columns of this tile
+      const int acc_cols = hn << wide;  // accumulator columns of this tile
       // full-sector (32-B) stores when the output rows are 32-B aligned
       const bool v8ok = ((reinterpret_cast<uintptr_t>(st.c) | (st.ldc * sizeof(T))) & 31) == 0;
       constexpr int G = C::kEpiGroups;
-      if (st.epilogue == TS_EPI_SWIGLU) {
+      if (st.splits > 1) {
+        // Split-K slice (the reference's z > 1) of a normal tile: publish this CTA's fp32
+        // partial rows, count arrivals per (tile, CTA); the last slice to arrive sums all
+        // partials, applies the epilogue and stores. Every slice still posts once below
+        // (consumers wait for expected x z), and each post follows its own stores, so
+        // the count only reaches its target after the summing slice has stored.
+        const int tile_id = t.tx * st.grid_y + t.ty;
+        const int rl_row = ew * 32 + lane;  // this thread's row inside the CTA's 128
+        // partial plane of one CTA: [acc_cols / 32 chunks][128 rows][32 floats], so a
+        // warp's 32 rows of one chunk are 4 KB contiguous (coalesced writes and reads)
+        const size_t plane = static_cast<size_t>(128) * acc_cols;
+        float* mine = st.ws + (static_cast<size_t>(tile_id * st.splits + t.tz) * CG + rank) * plane;
+        const int span = acc_cols / G;
+#pragma unroll 1
+        for (int j = 0; j <= wide; ++j) {
+          const int lo = max(eg * span, j * hn), hi = min((eg + 1) * span, (j + 1) * hn);
+#pragma unroll 1
+          for (int x = lo; x < hi; x += 32) {
+            uint32_t r[32];
+            ptx::tmem_ld_32x32b_x32(tcol(x), r);
+            ptx::tmem_ld_wait();
+            float* dst = mine + (static_cast<size_t>(x / 32) * 128 + rl_row) * 32;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ptx::st_global_v8(dst + 8 * q, r + 8 * q);
+          }
+          release_slot(j);
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        if (threadIdx.x == 128) {
+          const int half_id = tile_id * CG + static_cast<int>(rank);
+          const int old = atomicAdd(&st.cnt[half_id], 1);
+          *split_flag = (old == st.splits - 1);
+          if (old == st.splits - 1) st.cnt[half_id] = 0;  // restore the zero invariant
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        if (*split_flag) {
+          ptx::fence_acq_rel_gpu();
+          // Reduction, warp-cooperative: one step = 4 rows x 32 columns of one chunk
+          // (512 B per slice, lane l: row r0 + l / 8, columns (l % 8) * 4 .. + 4).
+          const float* base = st.ws + static_cast<size_t>(tile_id) * st.splits * CG * plane +
+                              static_cast<size_t>(rank) * plane;
+          const bool gl = st.epilogue == TS_EPI_GELU;
+          const bool rl = st.epilogue == TS_EPI_RELU;
+          const int steps = (acc_cols / 32) * 32;  // chunks x (128 rows / 4)
+          const int row0 = t.tx * C::kTileM + static_cast<int>(rank) * 128;
+#pragma unroll 1
+          for (int sidx = warp - 4; sidx < steps; sidx += kEpiWarps) {
+            const int chunk = sidx >> 5, r0 = (sidx & 31) * 4;
+            const size_t off = (static_cast<size_t>(chunk) * 128 + r0) * 32 + lane * 4;
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 v[4];
+#pragma unroll 1
+            for (int z0 = 0; z0 < st.splits; z0 += 4) {
+#pragma unroll
+              for (int zz = 0; zz < 4; ++zz)
+                v[zz] = z0 + zz < st.splits
+                            ? __ldcg(reinterpret_cast<const float4*>(base + (z0 + zz) * CG * plane + off))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int zz = 0; zz < 4; ++zz) {
+                a.x += v[zz].x;
+                a.y += v[zz].y;
+                a.z += v[zz].z;
+                a.w += v[zz].w;
+              }
+            }
+            float o[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) o[q] = gl ? gelu(o[q]) : (rl ? relu(o[q]) : o[q]);
+            const int grow = row0 + r0 + (lane >> 3);
+            if (grow < st.m) {
+              T* dst = reinterpret_cast<T*>(st.c) + static_cast<size_t>(grow) * st.ldc +
+                       t.ty * acc_cols + chunk * 32 + (lane & 7) * 4;
+              *reinterpret_cast<uint2*>(dst) = make_uint2(pack2<T>(o[0], o[1]), pack2<T>(o[2], o[3]));
+            }
+          }
+        }
+      } else if (st.epilogue == TS_EPI_SWIGLU) {
         // gate = accumulator columns [0, acc_cols/2), up = the matching upper half; each
         // column group stores its 1/G of the output columns
         const int half = acc_cols / 2;
@@ -989,7 +1074,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         const int span = acc_cols / G;
 #pragma unroll 1
         for (int j = 0; j <= wide; ++j) {
-          const int lo = max(eg * span, j * BN), hi = min((eg + 1) * span, (j + 1) * BN);
+          const int lo = max(eg * span, j * hn), hi = min((eg + 1) * span, (j + 1) * hn);
 #pragma unroll 1
           for (int x = lo; x < hi; x += 32) {
             uint32_t r[32];

@@ -153,6 +153,15 @@ class CuSync:
         swapped."""
         return self.tile_n if self.swap_ab else BM * self.cta_group
 
+    def _check_tile_n(self, tile_n: int) -> None:
+        """Per-stage tile width: 0 (the chain's), or 384 / 512 (two MMAs of 192 / 256
+        columns per K-block) on cta_group=2, tile_n=256 chains."""
+        if tile_n not in (0, self.tile_n) and not (
+                tile_n in (384, 512) and self.tile_n == 256 and self.cta_group == 2
+                and not self.swap_ab):
+            raise ConfigError(f"stage tile_n {tile_n} unsupported (0, {self.tile_n}, or "
+                              "384 / 512 with cta_group=2, tile_n=256)")
+
     # -- construction (PAPER.md:338-342) ---------------------------------------------
     def stage(self, a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, epilogue: str = "none",
               order: TileOrder = RowMajor(), id: str | None = None,
@@ -161,10 +170,7 @@ class CuSync:
         reference's z extent): each slice posts once, consumers wait for all of them.
         ``tile_n=512`` gives this stage double-width CTA-pair tiles (256 x 512 outputs;
         chains with ``cta_group=2, tile_n=256`` only)."""
-        if tile_n not in (0, self.tile_n) and not (
-                tile_n == 512 and self.tile_n == 256 and self.cta_group == 2 and not self.swap_ab):
-            raise ConfigError(f"stage tile_n {tile_n} unsupported (0, {self.tile_n}, or 512 "
-                              "with cta_group=2, tile_n=256)")
+        self._check_tile_n(tile_n)
         if len(self.stages) >= _lib.TS_MAX_STAGES:
             raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
         if epilogue not in _EPI:
@@ -186,10 +192,11 @@ class CuSync:
         st = CuStage(self, len(self.stages), id or f"gemm{len(self.stages) + 1}", a, b, c,
                      epilogue, order, splits, tile_n=tile_n)
         if splits > 1:
+            # fp32 partials [tile][slice][tile_m rows][width] and per-(tile, CTA) counters
             tiles = st.grid.x * st.grid.y
-            st.ws = torch.empty(tiles * splits * self.tile_n * 128, dtype=torch.float32,
+            st.ws = torch.empty(tiles * splits * self.tile_m * st.width, dtype=torch.float32,
                                 device=a.device)
-            st.cnt = torch.zeros(tiles, dtype=torch.int32, device=a.device)
+            st.cnt = torch.zeros(tiles * self.cta_group, dtype=torch.int32, device=a.device)
         self.stages.append(st)
         self.device = a.device
         self._desc = None
@@ -236,9 +243,7 @@ class CuSync:
         if w.shape[3] != cin or tuple(out.shape) != (n, h, wd, w.shape[0]):
             raise ValueError(f"shape mismatch: x {tuple(x.shape)} w {tuple(w.shape)} "
                              f"out {tuple(out.shape)}")
-        if tile_n not in (0, self.tile_n) and not (
-                tile_n == 512 and self.tile_n == 256 and self.cta_group == 2 and not self.swap_ab):
-            raise ConfigError(f"stage tile_n {tile_n} unsupported")
+        self._check_tile_n(tile_n)
         st = CuStage(self, len(self.stages), id or f"conv{len(self.stages) + 1}",
                      x.view(n * h * wd, cin), w.reshape(w.shape[0], 9 * cin),
                      out.view(n * h * wd, w.shape[0]), epilogue, order, kind="conv",

@@ -131,11 +131,13 @@ def main():
         mode, pol, po, co = parts[:4]
         flags = int(parts[4], 0) if len(parts) > 4 else 0
         swap_tn = int(parts[5]) if len(parts) > 5 else 0
-        splits = int(parts[6]) if len(parts) > 6 else 1
+        zs = [int(z) for z in parts[6].split("/")] if len(parts) > 6 else [1]
+        z1, z2 = zs[0], (zs[1] if len(zs) > 1 else 1)
         widths = [int(w) for w in parts[7].split("/")] if len(parts) > 7 else [0, 0]
         policy = {"row": ts.RowSync(), "tile": ts.TileSync()}[pol]
-        kw = dict(swap_ab=True, tile_n=swap_tn, prod_splits=splits) if swap_tn else \
-            dict(prod_tile_n=widths[0], cons_tile_n=widths[1])
+        kw = dict(prod_splits=z1, cons_splits=z2)
+        kw.update(dict(swap_ab=True, tile_n=swap_tn) if swap_tn else
+                  dict(prod_tile_n=widths[0], cons_tile_n=widths[1]))
         ch = ts.MlpChain(x, w1, w2, policy=policy, mode=mode, prod_order=order(po),
                          cons_order=order(co), extra_flags=flags, **kw)
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)

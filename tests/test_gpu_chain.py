@@ -319,6 +319,9 @@ WIDE_CASES = [
     (520, 512, 512, 1024, 512, 256, ts.TileSync(), "fused"),
     (700, 1024, 1536, 1024, 512, 512, ts.RowSync(), "stream"),
     (64, 512, 1024, 512, 512, 256, ts.Conv2DTileSync(4), "fused"),
+    (300, 768, 768, 768, 384, 384, ts.RowSync(), "fused"),
+    (520, 512, 1536, 1024, 384, 512, ts.TileSync(), "fused"),
+    (256, 1024, 768, 768, 256, 384, ts.RowSync(), "stream"),
 ]
 
 
@@ -341,16 +344,16 @@ def test_double_width_numerics(m, k, n1, n2, pt, ct, pol, mode, dtype):
 
 
 @pytest.mark.parametrize("pol", [ts.RowSync(), ts.TileSync()])
-@pytest.mark.parametrize("pt,ct", [(512, 512), (256, 512), (512, 256)])
+@pytest.mark.parametrize("pt,ct", [(512, 512), (256, 512), (512, 256), (384, 384)])
 def test_double_width_trace_parity(pol, pt, ct):
-    x, w1, w2 = make(600, 512, 2048, 1024, seed=9)
+    x, w1, w2 = make(600, 512, 1536 if pt == 384 else 2048, 768 if ct == 384 else 1024, seed=9)
     ch = ts.MlpChain(x.cuda(), w1.cuda(), w2.cuda(), policy=pol, tile_n=256, cta_group=2,
                      keep_sems=True, prod_tile_n=pt, cons_tile_n=ct)
     ch.cs.enable_trace()
     ch()
     torch.cuda.synchronize()
     stages, deps = _scenario_dicts(ch.cs)
-    assert stages[0]["grid"][1] == 2048 // pt and stages[1]["grid"][1] == 1024 // ct
+    assert stages[0]["grid"][1] == w1.shape[0] // pt and stages[1]["grid"][1] == w2.shape[0] // ct
     evs = ch.cs.trace_events()
     ev_dicts = [{"t": e.time, "stage": e.stage, "tb": e.tb, "kind": e.kind,
                  "tile": list(e.tile), "k": e.k, "dep": e.dep, "sem": e.sem,
@@ -380,3 +383,56 @@ def test_double_width_swiglu():
                                   wd.float().numpy(), "bf16")
     check_close(ch.h, h_ref, torch.bfloat16)
     check_close(y, y_ref, torch.bfloat16)
+
+
+SPLIT_CASES = [
+    # m, k, n1, n2, cta_group, prod_tile_n, cons_tile_n, z1, z2, policy, mode
+    (256, 1536, 512, 512, 2, 0, 0, 3, 1, ts.RowSync(), "fused"),
+    (300, 1024, 1024, 512, 2, 512, 0, 2, 2, ts.TileSync(), "fused"),
+    (520, 768, 512, 1024, 2, 512, 512, 3, 2, ts.RowSync(), "fused"),
+    (200, 1024, 512, 256, 1, 0, 0, 4, 2, ts.TileSync(), "fused"),
+    (260, 1024, 512, 512, 2, 0, 512, 2, 1, ts.RowSync(), "stream"),
+]
+
+
+@pytest.mark.parametrize("m,k,n1,n2,cg,pt,ct,z1,z2,pol,mode", SPLIT_CASES)
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_normal_split_numerics(m, k, n1, n2, cg, pt, ct, z1, z2, pol, mode, dtype):
+    """Split-K slices (reference z > 1) of normal and double-width tiles: each slice
+    publishes fp32 partials, the last arriver per (tile, CTA) reduces and stores."""
+    x, w1, w2 = make(m, k, n1, n2, dtype, seed=13)
+    ch = ts.MlpChain(x.cuda(), w1.cuda(), w2.cuda(), policy=pol, mode=mode, tile_n=256,
+                     cta_group=cg, prod_tile_n=pt, cons_tile_n=ct, prod_splits=z1,
+                     cons_splits=z2)
+    for _ in range(3):
+        y = ch()
+    torch.cuda.synchronize()
+    assert not ch.cs.watchdog_fired()
+    h_ref, y_ref = oracle_mlp(x, w1, w2, dtype)
+    check_close(ch.h, h_ref, dtype)
+    check_close(y, y_ref, dtype)
+    for st in ch.cs.stages:
+        if st.cnt is not None:
+            assert int(st.cnt.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("pol", [ts.RowSync(), ts.TileSync()])
+def test_normal_split_trace_parity(pol):
+    x, w1, w2 = make(600, 1536, 1024, 512, seed=17)
+    ch = ts.MlpChain(x.cuda(), w1.cuda(), w2.cuda(), policy=pol, tile_n=256, cta_group=2,
+                     prod_tile_n=512, prod_splits=3, cons_splits=2, keep_sems=True)
+    ch.cs.enable_trace()
+    ch()
+    torch.cuda.synchronize()
+    stages, deps = _scenario_dicts(ch.cs)
+    evs = ch.cs.trace_events()
+    ev_dicts = [{"t": e.time, "stage": e.stage, "tb": e.tb, "kind": e.kind,
+                 "tile": list(e.tile), "k": e.k, "dep": e.dep, "sem": e.sem,
+                 "expected": e.expected} for e in evs]
+    assert O.validate_trace(ev_dicts, stages, deps, fine=True) == []
+    final = ch.cs.final_semaphores()
+    assert {k: tuple(v) for k, v in O.final_semaphores(stages, deps).items()} == final
+    g1 = stages[0]["grid"]
+    assert sum(1 for e in evs if e.kind == "post") == g1[0] * g1[1] * g1[2]
+    _, y_ref = oracle_mlp(x, w1, w2, torch.float16)
+    check_close(ch.y, y_ref, torch.float16)
