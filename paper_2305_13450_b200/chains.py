@@ -103,7 +103,11 @@ class AttentionChain:
     def __init__(self, x: torch.Tensor, w_qkv: torch.Tensor, w2: torch.Tensor,
                  second_policy: SyncPolicy | None = None, mode: str = "fused",
                  cta_group: int = 2, keep_sems: bool = False, num_ctas: int = 0,
-                 extra_flags: int = 0, tile_n: int = 256):
+                 extra_flags: int = 0, tile_n: int = 256, qkv_splits: int = 1,
+                 out_splits: int = 1):
+        """``qkv_splits`` / ``out_splits`` > 1 split the GeMMs' K into reference z-slices
+        (each posts once; StridedSync/TileSync expect x z) — the QKV GeMM of a short
+        sequence has too few output tiles to fill 148 SMs otherwise."""
         from .policies import StridedRowMajor, StridedSync, TileSync
         m = x.shape[0]
         n3 = w_qkv.shape[0]
@@ -117,9 +121,10 @@ class AttentionChain:
         self.y = torch.empty(m, w2.shape[0], dtype=x.dtype, device=x.device)
         self.cs = CuSync(tile_n=tile_n, mode=mode, cta_group=cta_group, keep_sems=keep_sems,
                          num_ctas=num_ctas, extra_flags=extra_flags)
-        self.s_qkv = self.cs.stage(x, w_qkv, self.qkv, order=StridedRowMajor(stride), id="qkv")
+        self.s_qkv = self.cs.stage(x, w_qkv, self.qkv, order=StridedRowMajor(stride), id="qkv",
+                                   splits=qkv_splits)
         self.s_dot = self.cs.stage_dot(self.qkv, self.dot, id="dot")
-        self.s_out = self.cs.stage(self.dot, w2, self.y, id="out")
+        self.s_out = self.cs.stage(self.dot, w2, self.y, id="out", splits=out_splits)
         self.cs.dependency(StridedSync(stride), self.s_qkv, self.s_dot, operand="qkv")
         self.cs.dependency(second_policy or TileSync(), self.s_dot, self.s_out, operand="a")
 

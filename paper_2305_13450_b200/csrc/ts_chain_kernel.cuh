@@ -45,6 +45,12 @@ constexpr int kTileRing = 4;    // tile-id hand-off ring between scheduler and c
 // 16-KB chunks, 1-3 per K-block) is independent of the barriers.
 constexpr int kFullRing = 16;    // > K-blocks in flight (<= 13)
 constexpr int kCommitRing = 16;  // > commit groups in flight
+// CTA pairs: the peer's "my stores of tile i are done" barrier ring. The peer's epilogue
+// can run up to two tiles ahead of the leader's post (bounded by the two TMEM slots), so
+// a 2-entry ring could see two phases complete before the leader waits — parity aliasing
+// (observed as hangs when the leader's epilogue is slowed by split-K reductions or
+// last-arriver dot tiles). Four entries keep every outstanding tile on its own barrier.
+constexpr int kPeerRing = 4;
 constexpr uint64_t kWatchdogNs = 4000000000ull;
 constexpr int kStageGemm = 0;  // C = epi(A x B^T) on tcgen05
 constexpr int kStageDot = 1;   // attention's fused softmax-dot over QKV column tiles
@@ -152,9 +158,8 @@ struct Cfg {
   static constexpr int kTmemCols = 2 * kAccCols;       // two tile buffers
   static constexpr int kRing = kChunked ? kChunks : kStages;  // ring entries
   static constexpr int kBarOffset = kChunked ? kChunks * kChunkBytes : kStages * kStageBytes;
-  // K-block full, commit-group empty; tmem full/empty x2; tile ring full/empty; peer_done x2
-  static constexpr int kNumBars = kFullRing + kCommitRing + 4 + 2 * kTileRing + 2;
-  // + tile ring ids, TMEM slot, flags and the last-arriver dot list (64 ints)
+  // K-block full, commit-group empty; tmem full/empty x2; tile ring full/empty; peer_done
+  static constexpr int kNumBars = kFullRing + kCommitRing + 4 + 2 * kTileRing + kPeerRing;
   // + tile ring ids, TMEM slot, flags and the last-arriver dot list (64 ints), ring-entry
   // owners (commit group that last read each entry)
   static constexpr int kSmemBytes = 1024 + kBarOffset + kNumBars * 8 + 64 + 272 + 4 * kRing;
@@ -368,7 +373,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
   uint64_t* ti_full = tmem_empty + 2;
   uint64_t* ti_empty = ti_full + kTileRing;
   uint64_t* peer_done = ti_empty + kTileRing;
-  int* ti_item = reinterpret_cast<int*>(peer_done + 2);
+  int* ti_item = reinterpret_cast<int*>(peer_done + kPeerRing);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ti_item + kTileRing);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   int* split_flag = last_flag + 1;
@@ -388,8 +393,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tmem_full[i], 1);
       ptx::mbar_init(&tmem_empty[i], CG * kEpiWarps);
-      ptx::mbar_init(&peer_done[i], 1);
     }
+    for (int i = 0; i < kPeerRing; ++i) ptx::mbar_init(&peer_done[i], 1);
     for (int i = 0; i < kTileRing; ++i) {
       ptx::mbar_init(&ti_full[i], 1);
       // leader MMA warp + every epilogue warp of the pair + the peer's producer lane
@@ -682,7 +687,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         for (int kb = 0, gi = 0; kb < kblocks; ++kb) {
           uint64_t* fb = &full[kq % kFullRing];
           const uint32_t ph = (kq / kFullRing) & 1;
-          if (tr && !ptx::mbar_test_wait(fb, ph)) {
+          if ((p.flags >> 19) & 1) {
+            // diagnostic only (flag bit 19): MMA pipe rate without waiting for operands
+          } else if (tr && !ptx::mbar_test_wait(fb, ph)) {
             const uint64_t t0 = ptx::global_timer();
             ptx::mbar_wait(fb, ph);
             if (kb > 0) starve_ns += ptx::global_timer() - t0;
@@ -712,13 +719,17 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
               const uint32_t b_addr = ptx::smem_u32(sB + rs * C::kBBytes);
               if (no_mma) {
               } else if constexpr (C::kAcc > 1) {
+                // rotate independent accumulators (sub-step `step` -> step % kAcc), the
+                // K-block's four MMAs in one issue sequence
+                const int step = kb * (kBK / 16);
+                uint32_t dd[4], mask = 0;
 #pragma unroll
-                for (int k = 0; k < kBK / 16; ++k) {
-                  const uint64_t ad = ptx::smem_desc_k_sw128(a_addr + k * 32);
-                  const uint64_t bd = ptx::smem_desc_k_sw128(b_addr + k * 32);
-                  const int step = kb * (kBK / 16) + k;  // rotate independent accumulators
-                  ptx::umma_f16(d_tmem + (step % C::kAcc) * BN, ad, bd, kIdesc, step >= C::kAcc);
+                for (int k = 0; k < 4; ++k) {
+                  dd[k] = d_tmem + ((step + k) % C::kAcc) * BN;
+                  mask |= (step + k >= C::kAcc ? 1u : 0u) << k;
                 }
+                ptx::umma_f16_kblock4(dd[0], dd[1], dd[2], dd[3], ptx::smem_desc_k_sw128(a_addr),
+                                      ptx::smem_desc_k_sw128(b_addr), kIdesc, mask);
               } else {
                 // the K-block's four MMAs back to back in one issue sequence
                 ptx::umma_f16_kblock<CG>(d_tmem, ptx::smem_desc_k_sw128(a_addr),
@@ -770,13 +781,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
     const int eg = (warp - 4) >> 2;  // column group (chunked tiles: 0 or 1)
     uint32_t local = 0;  // GeMM tiles (peer_done parity)
     uint32_t u = 0;      // TMEM accumulator-slot uses, as counted by the MMA warp
-    uint32_t tmem_empty_remote[2] = {0, 0}, peer_done_remote[2] = {0, 0};
+    uint32_t tmem_empty_remote[2] = {0, 0};
     if constexpr (CG == 2) {
       if (!leader) {
-        for (int i = 0; i < 2; ++i) {
-          tmem_empty_remote[i] = ptx::mapa(&tmem_empty[i], 0);
-          peer_done_remote[i] = ptx::mapa(&peer_done[i], 0);
-        }
+        for (int i = 0; i < 2; ++i) tmem_empty_remote[i] = ptx::mapa(&tmem_empty[i], 0);
       }
     }
     // Compute dot tile (tx, ty) of stage ds with the 128 epilogue threads (its wait is
@@ -836,7 +844,6 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         run_dot(t.s, t.tx, t.ty, t.tb);
         continue;
       }
-      const uint32_t acc = local & 1;
       const int wide = C::kChunked ? st.wide : 0;
       const int hn = C::kChunked ? st.half_n : BN;  // accumulator columns per slot
       for (int j = 0; j <= wide; ++j)  // arrived by the MMA commits
@@ -1107,9 +1114,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       if (threadIdx.x == 128) {
         if (CG == 2 && !leader) {
           __threadfence();
-          ptx::mbar_arrive_remote(peer_done_remote[acc]);
+          ptx::mbar_arrive_remote(ptx::mapa(&peer_done[local % kPeerRing], 0));
         } else {
-          if constexpr (CG == 2) ptx::mbar_wait_cluster(&peer_done[acc], (local >> 1) & 1);
+          if constexpr (CG == 2)
+            ptx::mbar_wait_cluster(&peer_done[local % kPeerRing], (local / kPeerRing) & 1);
           const uint64_t tnow = ptx::global_timer();
           if (st.n_out_deps > 0) {
             __threadfence();

@@ -344,6 +344,27 @@ __device__ __forceinline__ void umma_f16_kblock(uint32_t d_tmem, uint64_t adesc,
   }
 }
 
+// Four K=16 sub-steps of one K-block into four (possibly different) accumulators
+// d0..d3 with per-sub-step accumulate flags, in one issue sequence (single CTA).
+__device__ __forceinline__ void umma_f16_kblock4(uint32_t d0, uint32_t d1, uint32_t d2,
+                                                 uint32_t d3, uint64_t adesc, uint64_t bdesc,
+                                                 uint32_t idesc, uint32_t accmask) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1, p2, p3;\n\t"
+      "setp.ne.b32 p0, %8, 0;\n\t"
+      "setp.ne.b32 p1, %9, 0;\n\t"
+      "setp.ne.b32 p2, %10, 0;\n\t"
+      "setp.ne.b32 p3, %11, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %5, %6, p0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%1], %12, %13, %6, p1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%2], %14, %15, %6, p2;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%3], %16, %17, %6, p3;\n\t}" ::"r"(d0),
+      "r"(d1), "r"(d2), "r"(d3), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(0),
+      "r"(accmask & 1), "r"(accmask & 2), "r"(accmask & 4), "r"(accmask & 8), "l"(adesc + 2),
+      "l"(bdesc + 2), "l"(adesc + 4), "l"(bdesc + 4), "l"(adesc + 6), "l"(bdesc + 6)
+      : "memory");
+}
+
 // Arrive on `bar` once every previously issued tcgen05.mma of this thread completes.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(

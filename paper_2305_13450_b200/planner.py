@@ -45,7 +45,7 @@ def candidates(m: int, mode: str):
     pols = [RowSync(), TileSync()] if mode == "fused" else [RowSync()]
     if m <= 256:
         tn = next(t for t in (32, 64, 128, 256) if t >= m)
-        for z1, z2 in ((3, 1), (3, 2), (2, 2), (2, 1), (1, 1)):
+        for z1, z2 in ((3, 3), (3, 1), (6, 3), (3, 2), (2, 2), (1, 1)):
             for pol in pols:
                 out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=1, swap_ab=True,
                                 prod_splits=z1, cons_splits=z2))
@@ -132,12 +132,14 @@ def sweep_attention(seqs=(512, 1024, 2048), hidden=12288, heads=12, device=None)
         x = torch.randn(s, hidden, device=device).half()
         best = {}
         for mode in ("fused", "stream"):
-            for cg in (1, 2):
+            for cg, z in itertools.product((1, 2), (1, 2, 4)):
                 for pol in ([RowSync(), TileSync()] if mode == "fused" else [TileSync()]):
-                    ch = AttentionChain(x, wqkv, w2, second_policy=pol, mode=mode, cta_group=cg)
+                    ch = AttentionChain(x, wqkv, w2, second_policy=pol, mode=mode, cta_group=cg,
+                                        qkv_splits=z)
                     us = _time(ch, iters=20)
                     if us < best.get(mode, (float("inf"),))[0]:
-                        best[mode] = (us, {"cta_group": cg, "policy": type(pol).__name__})
+                        best[mode] = (us, {"cta_group": cg, "policy": type(pol).__name__,
+                                           "qkv_splits": z})
         cu = _time(lambda: _torch_attention(x, wqkv, w2, heads), iters=20)
         flops = 2 * s * hidden * 3 * heads * 128 + 2 * s * heads * 128 * hidden
         rows.append({"seq": s, "fused_us": best["fused"][0], "stream_us": best["stream"][0],

@@ -261,13 +261,15 @@ def test_split_trace_counts_follow_reference_z(pol, z1, z2):
         cons_slices * sum(n for (_, n) in dag.values())
 
 
-@pytest.mark.parametrize("m,heads,cg,mode,tn", [(256, 2, 2, "fused", 256),
-                                               (300, 3, 1, "fused", 128),
-                                               (520, 2, 2, "stream", 256),
-                                               (128, 4, 1, "fused", 256),
-                                               (200, 4, 2, "fused", 128)])
+@pytest.mark.parametrize("m,heads,cg,mode,tn,z", [(256, 2, 2, "fused", 256, 1),
+                                                 (300, 3, 1, "fused", 128, 1),
+                                                 (520, 2, 2, "stream", 256, 1),
+                                                 (128, 4, 1, "fused", 256, 1),
+                                                 (200, 4, 2, "fused", 128, 1),
+                                                 (256, 2, 2, "fused", 256, 4),
+                                                 (300, 3, 1, "fused", 128, 2)])
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
-def test_attention_chain(m, heads, cg, mode, tn, dtype):
+def test_attention_chain(m, heads, cg, mode, tn, z, dtype):
     """QKV (StridedRowMajor) -> fused dot (StridedSync) -> out GeMM (TileSync)."""
     g = torch.Generator().manual_seed(11)
     h = 512
@@ -275,7 +277,7 @@ def test_attention_chain(m, heads, cg, mode, tn, dtype):
     wqkv = (torch.randn(3 * heads * 128, h, generator=g) / h ** 0.5).to(dtype)
     w2 = (torch.randn(h, heads * 128, generator=g) / (heads * 128) ** 0.5).to(dtype)
     ch = ts.AttentionChain(x.cuda(), wqkv.cuda(), w2.cuda(), mode=mode, cta_group=cg,
-                           keep_sems=(mode == "fused"), tile_n=tn)
+                           keep_sems=(mode == "fused"), tile_n=tn, qkv_splits=z)
     ch.cs.enable_trace()
     ch()
     torch.cuda.synchronize()
@@ -306,7 +308,7 @@ def test_attention_chain(m, heads, cg, mode, tn, dtype):
             continue  # last-arriver dot tiles are claimed in completion order
         for e in sched:
             t = ts.order_tile(st.order, st.grid, e["tb"])
-            assert tuple(e["tile"]) == (t.x, t.y, 0)
+            assert tuple(e["tile"]) == (t.x, t.y, t.z)
     if mode == "fused":
         assert {k: tuple(v) for k, v in O.final_semaphores(stages, deps).items()} == \
             ch.cs.final_semaphores()
