@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--plan", choices=["auto", "fixed"], default="auto",
+                    help="auto: time the planner's candidates; fixed: the B=1024 headline "
+                         "configuration without the search (for profiling runs)")
     return ap.parse_args()
 
 
@@ -226,8 +229,14 @@ def main():
     flops = 2 * b * H * FFN * 2
 
     # co-scheduling choice (policy, tile order, CTA group) from measured candidates
-    best, cands = planner.pick_mlp(x, w1, w2, mode="fused")
-    base, bcands = planner.pick_mlp(x, w1, w2, mode="stream")
+    if args.plan == "auto":
+        best, cands = planner.pick_mlp(x, w1, w2, mode="fused")
+        base, bcands = planner.pick_mlp(x, w1, w2, mode="stream")
+    else:
+        fixed = dict(policy=ts.RowSync(), tile_n=256, cta_group=2, prod_tile_n=512,
+                     cons_tile_n=512, cons_order=ts.BandedColumnMajor(4))
+        best, cands = dict(fixed, mode="fused"), []
+        base, bcands = dict(fixed, mode="stream"), []
     chain = ts.MlpChain(x, w1, w2, **best)
     stream_chain = ts.MlpChain(x, w1, w2, **base)
 
