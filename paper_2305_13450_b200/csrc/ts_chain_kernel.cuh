@@ -276,50 +276,61 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   for (int j = 0; j < 8; ++j) f[j] = static_cast<float>(h[j]);
 }
 
-// One row of the fused softmax-dot for head `h`: s = q*v (elementwise over the head's
-// 128 columns), p = softmax(s), out = p*k. Q, K, V are the head's column tiles at
-// offsets h, heads + h and 2*heads + h (x128) of the QKV row.
+// The fused softmax-dot for kDotBatch (row, head) items, one warp per item: s = q*v over
+// the head's 128 columns (4 per lane), p = softmax(s) (warp-shuffle max and sum), out =
+// p*k. Q, K, V are the head's column tiles at offsets h, heads + h and 2*heads + h (x128)
+// of the QKV row; reads are coalesced 256-B rows through L2 (written by other SMs). All
+// loads of the batch are issued before any is used: under a streaming GeMM the loaded L2
+// latency is microseconds, and one item in flight made a 128 x 256 dot tile take ~40 us.
+constexpr int kDotBatch = 4;
 template <typename T>
-__device__ __forceinline__ void dot_row(const StageParams& st, int row, int h) {
+__device__ __forceinline__ void dot_batch_warp(const StageParams& st, int row0, int rstep,
+                                               int hcount, int it0, int istep, int items,
+                                               int h0, int lane) {
   const int heads = st.n / 128;
-  const T* base = reinterpret_cast<const T*>(st.a) + static_cast<size_t>(row) * st.lda;
-  const uint4* q = reinterpret_cast<const uint4*>(base + h * 128);
-  const uint4* k = reinterpret_cast<const uint4*>(base + (heads + h) * 128);
-  const uint4* v = reinterpret_cast<const uint4*>(base + (2 * heads + h) * 128);
-  uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<T*>(st.c) +
-                                        static_cast<size_t>(row) * st.ldc + h * 128);
-  float mx = -INFINITY, sum = 0.f;
-#pragma unroll 4
-  for (int j = 0; j < 16; ++j) {
-    float qf[8], vf[8];
-    unpack8<T>(__ldcg(q + j), qf);
-    unpack8<T>(__ldcg(v + j), vf);
+  uint2 qv[kDotBatch], kv[kDotBatch], vv[kDotBatch];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float s = qf[e] * vf[e];
-      if (s > mx) {
-        sum = sum * __expf(mx - s) + 1.f;
-        mx = s;
-      } else {
-        sum += __expf(s - mx);
-      }
+  for (int i = 0; i < kDotBatch; ++i) {
+    const int it = it0 + i * istep;
+    const int row = row0 + (it / hcount) * rstep;
+    if (it < items && row < st.m) {
+      const int h = h0 + it % hcount;
+      const T* base = reinterpret_cast<const T*>(st.a) + static_cast<size_t>(row) * st.lda + lane * 4;
+      qv[i] = __ldcg(reinterpret_cast<const uint2*>(base + h * 128));
+      kv[i] = __ldcg(reinterpret_cast<const uint2*>(base + (heads + h) * 128));
+      vv[i] = __ldcg(reinterpret_cast<const uint2*>(base + (2 * heads + h) * 128));
     }
   }
-  const float inv = 1.f / sum;
-#pragma unroll 4
-  for (int j = 0; j < 16; ++j) {
-    float qf[8], vf[8], kf[8];
-    unpack8<T>(__ldcg(q + j), qf);
-    unpack8<T>(__ldcg(v + j), vf);
-    unpack8<T>(__ldcg(k + j), kf);
-    uint32_t pk[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float o0 = __expf(qf[2 * e] * vf[2 * e] - mx) * inv * kf[2 * e];
-      const float o1 = __expf(qf[2 * e + 1] * vf[2 * e + 1] - mx) * inv * kf[2 * e + 1];
-      pk[e] = pack2<T>(o0, o1);
+  for (int i = 0; i < kDotBatch; ++i) {
+    const int it = it0 + i * istep;
+    const int row = row0 + (it / hcount) * rstep;
+    if (it >= items || row >= st.m) continue;
+    const int h = h0 + it % hcount;
+    const T* q = reinterpret_cast<const T*>(&qv[i]);
+    const T* k = reinterpret_cast<const T*>(&kv[i]);
+    const T* v = reinterpret_cast<const T*>(&vv[i]);
+    float sc[4], mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      sc[j] = static_cast<float>(q[j]) * static_cast<float>(v[j]);
+      mx = fmaxf(mx, sc[j]);
     }
-    out[j] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      sc[j] = __expf(sc[j] - mx);
+      sum += sc[j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float inv = 1.f / sum;
+    T* out = reinterpret_cast<T*>(st.c) + static_cast<size_t>(row) * st.ldc + h * 128 + lane * 4;
+    *reinterpret_cast<uint2*>(out) = make_uint2(
+        pack2<T>(sc[0] * inv * static_cast<float>(k[0]), sc[1] * inv * static_cast<float>(k[1])),
+        pack2<T>(sc[2] * inv * static_cast<float>(k[2]), sc[3] * inv * static_cast<float>(k[3])));
   }
 }
 
@@ -793,18 +804,18 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       const StageParams& sd = p.st[ds];
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
       ptx::fence_acq_rel_gpu();
+      if (threadIdx.x == 128) trace_event(p, ptx::global_timer(), 7, ds, tb, -1, -1, -1, -1, tx, ty);
+      // a dot tile covers BN / 128 heads (the paper's stride H / (8 Ty));
+      // one warp per (row, head), warps striding over the tile's rows x heads
+      constexpr int kHeads = BN >= 128 ? BN / 128 : 1;
+      const int items = C::kTileM * kHeads;
 #pragma unroll 1
-      for (int rr = (warp - 4) * 32 + lane; rr < C::kTileM; rr += kEpiThreads) {
-        const int row = tx * C::kTileM + rr;
-        if (row < sd.m) {
-          // a dot tile covers BN / 128 heads (the paper's stride H / (8 Ty))
-#pragma unroll 1
-          for (int hh = 0; hh < BN / 128; ++hh) dot_row<T>(sd, row, ty * (BN / 128) + hh);
-        }
-      }
+      for (int it0 = warp - 4; it0 < items; it0 += kEpiWarps * kDotBatch)
+        dot_batch_warp<T>(sd, tx * C::kTileM, 1, kHeads, it0, kEpiWarps, items, ty * kHeads, lane);
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
       if (threadIdx.x == 128) {
         const uint64_t tnow = ptx::global_timer();
+        trace_event(p, tnow, 8, ds, tb, -1, -1, -1, -1, tx, ty);
         __threadfence();
         ptx::fence_proxy_async_global();
         for (int i = 0; i < sd.n_out_deps; ++i) {

@@ -72,9 +72,11 @@ def summarize(cs, label):
     for s_i, st in enumerate(cs.stages):
         d = [ee[k] - eb[k] for k in eb if k[0] == s_i and k in ee]
         lag = [eb[k] - me[k].t_ns for k in eb if k[0] == s_i and k in me]
-        if d:
+        if d and lag:
             print(f"  {st.id}: epilogue mean {sum(d) / len(d) / 1e3:.1f} us (last MMA issue -> "
                   f"accumulator ready {sum(lag) / len(lag) / 1e3:.1f} us)")
+        elif d:
+            print(f"  {st.id}: compute mean {sum(d) / len(d) / 1e3:.1f} us")
     # MMA idle per CTA(-pair leader): before its first tile, between tiles, after its last
     per_sm = defaultdict(list)
     for k, r in me.items():
