@@ -276,61 +276,66 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   for (int j = 0; j < 8; ++j) f[j] = static_cast<float>(h[j]);
 }
 
-// The fused softmax-dot for kDotBatch (row, head) items, one warp per item: s = q*v over
-// the head's 128 columns (4 per lane), p = softmax(s) (warp-shuffle max and sum), out =
-// p*k. Q, K, V are the head's column tiles at offsets h, heads + h and 2*heads + h (x128)
-// of the QKV row; reads are coalesced 256-B rows through L2 (written by other SMs). All
-// loads of the batch are issued before any is used: under a streaming GeMM the loaded L2
-// latency is microseconds, and one item in flight made a 128 x 256 dot tile take ~40 us.
-constexpr int kDotBatch = 4;
-template <typename T>
-__device__ __forceinline__ void dot_batch_warp(const StageParams& st, int row0, int rstep,
-                                               int hcount, int it0, int istep, int items,
-                                               int h0, int lane) {
+// The fused softmax-dot, two (row, head) items per warp instruction (lanes 0-15: item
+// 2j, lanes 16-31: item 2j+1; 8 columns per lane), kDotBatch instruction pairs in flight:
+// s = q*v over the head's 128 columns, p = softmax(s) (16-lane shuffle max and sum),
+// out = p*k. Q, K, V are the head's column tiles at offsets h, heads + h and 2*heads + h
+// (x128) of the QKV row, read through L2 (written by other SMs). All loads of a batch are
+// issued before any is used: under a streaming GeMM the loaded L2 latency is ~1.5 us, and
+// one item in flight made a 128 x 256 dot tile take ~40 us.
+template <typename T, int kDotBatch>
+__device__ __forceinline__ void dot_batch_warp(const StageParams& st, int row0, int hcount,
+                                               int it0, int istep, int items, int h0,
+                                               int lane) {
   const int heads = st.n / 128;
-  uint2 qv[kDotBatch], kv[kDotBatch], vv[kDotBatch];
+  const int half = lane >> 4, col = (lane & 15) * 8;
+  uint4 qv[kDotBatch], kv[kDotBatch], vv[kDotBatch];
 #pragma unroll
   for (int i = 0; i < kDotBatch; ++i) {
-    const int it = it0 + i * istep;
-    const int row = row0 + (it / hcount) * rstep;
+    const int it = it0 + i * istep + half;
+    const int row = row0 + it / hcount;
     if (it < items && row < st.m) {
       const int h = h0 + it % hcount;
-      const T* base = reinterpret_cast<const T*>(st.a) + static_cast<size_t>(row) * st.lda + lane * 4;
-      qv[i] = __ldcg(reinterpret_cast<const uint2*>(base + h * 128));
-      kv[i] = __ldcg(reinterpret_cast<const uint2*>(base + (heads + h) * 128));
-      vv[i] = __ldcg(reinterpret_cast<const uint2*>(base + (2 * heads + h) * 128));
+      const T* base = reinterpret_cast<const T*>(st.a) + static_cast<size_t>(row) * st.lda + col;
+      qv[i] = __ldcg(reinterpret_cast<const uint4*>(base + h * 128));
+      kv[i] = __ldcg(reinterpret_cast<const uint4*>(base + (heads + h) * 128));
+      vv[i] = __ldcg(reinterpret_cast<const uint4*>(base + (2 * heads + h) * 128));
     }
   }
 #pragma unroll
   for (int i = 0; i < kDotBatch; ++i) {
-    const int it = it0 + i * istep;
-    const int row = row0 + (it / hcount) * rstep;
-    if (it >= items || row >= st.m) continue;
-    const int h = h0 + it % hcount;
+    const int it = it0 + i * istep + half;
+    const int row = row0 + it / hcount;
+    const bool ok = it < items && row < st.m;  // the two half-warps shuffle separately
     const T* q = reinterpret_cast<const T*>(&qv[i]);
     const T* k = reinterpret_cast<const T*>(&kv[i]);
     const T* v = reinterpret_cast<const T*>(&vv[i]);
-    float sc[4], mx = -INFINITY;
+    float sc[8], mx = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      sc[j] = static_cast<float>(q[j]) * static_cast<float>(v[j]);
+    for (int j = 0; j < 8; ++j) {
+      sc[j] = ok ? static_cast<float>(q[j]) * static_cast<float>(v[j]) : 0.f;
       mx = fmaxf(mx, sc[j]);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     float sum = 0.f;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 8; ++j) {
       sc[j] = __expf(sc[j] - mx);
       sum += sc[j];
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (!ok) continue;
     const float inv = 1.f / sum;
-    T* out = reinterpret_cast<T*>(st.c) + static_cast<size_t>(row) * st.ldc + h * 128 + lane * 4;
-    *reinterpret_cast<uint2*>(out) = make_uint2(
-        pack2<T>(sc[0] * inv * static_cast<float>(k[0]), sc[1] * inv * static_cast<float>(k[1])),
-        pack2<T>(sc[2] * inv * static_cast<float>(k[2]), sc[3] * inv * static_cast<float>(k[3])));
+    const int h = h0 + it % hcount;
+    uint32_t pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      pk[j] = pack2<T>(sc[2 * j] * inv * static_cast<float>(k[2 * j]),
+                       sc[2 * j + 1] * inv * static_cast<float>(k[2 * j + 1]));
+    T* out = reinterpret_cast<T*>(st.c) + static_cast<size_t>(row) * st.ldc + h * 128 + col;
+    *reinterpret_cast<uint4*>(out) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
   }
 }
 
@@ -809,9 +814,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       // one warp per (row, head), warps striding over the tile's rows x heads
       constexpr int kHeads = BN >= 128 ? BN / 128 : 1;
       const int items = C::kTileM * kHeads;
+      // loads in flight per warp: 2 x kB items (fewer for 384-thread CTAs, 168 registers)
+      constexpr int kB = C::kChunked ? 2 : 4;
 #pragma unroll 1
-      for (int it0 = warp - 4; it0 < items; it0 += kEpiWarps * kDotBatch)
-        dot_batch_warp<T>(sd, tx * C::kTileM, 1, kHeads, it0, kEpiWarps, items, ty * kHeads, lane);
+      for (int it0 = (warp - 4) * 2; it0 < items; it0 += kEpiWarps * 2 * kB)
+        dot_batch_warp<T, kB>(sd, tx * C::kTileM, kHeads, it0, kEpiWarps * 2, items, ty * kHeads, lane);
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
       if (threadIdx.x == 128) {
         const uint64_t tnow = ptx::global_timer();
