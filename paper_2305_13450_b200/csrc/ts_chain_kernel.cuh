@@ -1034,35 +1034,52 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           const bool rl = st.epilogue == TS_EPI_RELU;
           const int steps = (acc_cols / 32) * 32;  // chunks x (128 rows / 4)
           const int row0 = t.tx * C::kTileM + static_cast<int>(rank) * 128;
+          // kSB steps per iteration with every slice's load of every step in flight (the
+          // loop is L2-latency bound otherwise: ~1.5 us per round trip under load)
+          constexpr int kSB = C::kChunked ? 2 : 4;
 #pragma unroll 1
-          for (int sidx = warp - 4; sidx < steps; sidx += kEpiWarps) {
-            const int chunk = sidx >> 5, r0 = (sidx & 31) * 4;
-            const size_t off = (static_cast<size_t>(chunk) * 128 + r0) * 32 + lane * 4;
-            float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-            float4 v[4];
+          for (int s0 = warp - 4; s0 < steps; s0 += kEpiWarps * kSB) {
+            float4 a[kSB];
+#pragma unroll
+            for (int j = 0; j < kSB; ++j) a[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
             for (int z0 = 0; z0 < st.splits; z0 += 4) {
+              float4 v[kSB][4];
 #pragma unroll
-              for (int zz = 0; zz < 4; ++zz)
-                v[zz] = z0 + zz < st.splits
-                            ? __ldcg(reinterpret_cast<const float4*>(base + (z0 + zz) * CG * plane + off))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int j = 0; j < kSB; ++j) {
+                const int sidx = s0 + j * kEpiWarps;
+                const size_t off = (static_cast<size_t>(sidx >> 5) * 128 + (sidx & 31) * 4) * 32 + lane * 4;
 #pragma unroll
-              for (int zz = 0; zz < 4; ++zz) {
-                a.x += v[zz].x;
-                a.y += v[zz].y;
-                a.z += v[zz].z;
-                a.w += v[zz].w;
+                for (int zz = 0; zz < 4; ++zz)
+                  v[j][zz] = (sidx < steps && z0 + zz < st.splits)
+                                 ? __ldcg(reinterpret_cast<const float4*>(base + (z0 + zz) * CG * plane + off))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int j = 0; j < kSB; ++j) {
+#pragma unroll
+                for (int zz = 0; zz < 4; ++zz) {
+                  a[j].x += v[j][zz].x;
+                  a[j].y += v[j][zz].y;
+                  a[j].z += v[j][zz].z;
+                  a[j].w += v[j][zz].w;
+                }
               }
             }
-            float o[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) o[q] = gl ? gelu(o[q]) : (rl ? relu(o[q]) : o[q]);
-            const int grow = row0 + r0 + (lane >> 3);
-            if (grow < st.m) {
-              T* dst = reinterpret_cast<T*>(st.c) + static_cast<size_t>(grow) * st.ldc +
-                       t.ty * acc_cols + chunk * 32 + (lane & 7) * 4;
-              *reinterpret_cast<uint2*>(dst) = make_uint2(pack2<T>(o[0], o[1]), pack2<T>(o[2], o[3]));
+            for (int j = 0; j < kSB; ++j) {
+              const int sidx = s0 + j * kEpiWarps;
+              if (sidx >= steps) break;
+              const int chunk = sidx >> 5, r0 = (sidx & 31) * 4;
+              float o[4] = {a[j].x, a[j].y, a[j].z, a[j].w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) o[q] = gl ? gelu(o[q]) : (rl ? relu(o[q]) : o[q]);
+              const int grow = row0 + r0 + (lane >> 3);
+              if (grow < st.m) {
+                T* dst = reinterpret_cast<T*>(st.c) + static_cast<size_t>(grow) * st.ldc +
+                         t.ty * acc_cols + chunk * 32 + (lane & 7) * 4;
+                *reinterpret_cast<uint2*>(dst) = make_uint2(pack2<T>(o[0], o[1]), pack2<T>(o[2], o[3]));
+              }
             }
           }
         }
