@@ -286,13 +286,19 @@ def main():
     # Y -> pinned host, every step, inside the timed region
     xh = x.cpu().pin_memory()
     yh = torch.empty(b, H, dtype=torch.float16).pin_memory()
+    # the end-to-end chain completes rows in order (RowMajor consumer) so finished row
+    # units can leave over PCIe while later rows compute
+    e2e_chain = ts.MlpChain(x.clone(), w1, w2, **dict(best, cons_order=ts.RowMajor()))
 
     def step_e2e():
-        chain.x.copy_(xh, non_blocking=True)
-        y = chain()
         if use_dist:
+            chain.x.copy_(xh, non_blocking=True)
+            y = chain()
             dist.all_reduce(y)
-        yh.copy_(y, non_blocking=True)
+            yh.copy_(y, non_blocking=True)
+        else:
+            # row-chunked H2D / D2H overlapped with the chain through row semaphores
+            e2e_chain.run_host(xh, yh)
 
     us_e2e = time_steps(step_e2e, args.steps, args.warmup, torch, dist if use_dist else None)
 

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 2
+#define TS_ABI_VERSION 3
 
 /* ---- status codes ---------------------------------------------------------------- */
 typedef enum {
@@ -146,6 +146,15 @@ typedef struct {
                         256 x 512: 2 x N=256) sharing one A box — fewer operand bytes
                         per MAC than 256 x 256. GeMM and conv stages of cta_group 2,
                         tile_n 256 chains that do not feed a dot stage */
+  int* in_sem;       /* optional external gate on operand A (e.g. a chunked host->device
+                        copy signalled by ts_stream_signal): a tile in activation-row tile
+                        r waits in_sem[r] >= in_expected before its first A load; never
+                        zeroed by the kernel (callers advance in_expected per launch) */
+  int in_expected;
+  int* out_sem;      /* optional: each tile (and split-K slice) of activation-row tile r
+                        adds 1 to out_sem[r] after all its rows are stored (system-scope
+                        release), so a copy stream can ts_stream_wait for finished rows;
+                        never zeroed */
 } ts_stage_desc;
 
 typedef enum {
@@ -220,6 +229,15 @@ int ts_chain_grid(const ts_chain_desc* desc, int s, int* gx, int* gy);
 /* Paper's wait kernel: one thread on `stream` spins until every
  * flags[i] != 0 (each set by the producer's stage.start()). */
 int ts_wait_kernel_launch(const int* flags, int n, void* stream);
+
+/* Stream-ordered semaphore ops for overlapping copies with a chain (the paper's
+ * producer -> consumer tile signal, with a copy engine on one side). Both run on the
+ * stream's front end (cuStreamWriteValue32 / cuStreamWaitValue32), not on an SM, so they
+ * make progress while a persistent chain occupies every SM:
+ * ts_stream_signal writes `value` to *sem once the stream's earlier work (e.g. a copy)
+ * is complete and visible; ts_stream_wait blocks `stream` until *sem >= value. */
+int ts_stream_signal(int* sem, int value, void* stream);
+int ts_stream_wait(const int* sem, int value, void* stream);
 
 /* SM count of the current device. */
 int ts_device_sm_count(int* out);

@@ -35,7 +35,7 @@ EXPORTS = (
     "ts_abi_version", "ts_last_error", "ts_sem_count", "ts_post_target",
     "ts_consumer_wait", "ts_wait_steps", "ts_order_tile", "ts_avoid_wait_kernel",
     "ts_chain_launch", "ts_chain_grid", "ts_wait_kernel_launch",
-    "ts_device_sm_count",
+    "ts_device_sm_count", "ts_stream_signal", "ts_stream_wait",
 )
 
 
@@ -49,7 +49,8 @@ class StageDesc(ctypes.Structure):
         ("splits", ctypes.c_int), ("workspace", ctypes.c_void_p),
         ("counters", ctypes.c_void_p), ("kind", ctypes.c_int),
         ("conv_n", ctypes.c_int), ("conv_h", ctypes.c_int), ("conv_w", ctypes.c_int),
-        ("tile_n", ctypes.c_int),
+        ("tile_n", ctypes.c_int), ("in_sem", ctypes.c_void_p), ("in_expected", ctypes.c_int),
+        ("out_sem", ctypes.c_void_p),
     ]
 
 
@@ -112,12 +113,14 @@ def load() -> ctypes.CDLL:
         "ts_chain_grid": ([ctypes.POINTER(ChainDesc), i, ip, ip], i),
         "ts_wait_kernel_launch": ([ctypes.c_void_p, i, ctypes.c_void_p], i),
         "ts_device_sm_count": ([ip], i),
+        "ts_stream_signal": ([ctypes.c_void_p, i, ctypes.c_void_p], i),
+        "ts_stream_wait": ([ctypes.c_void_p, i, ctypes.c_void_p], i),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.ts_abi_version() != 2:
+    if lib.ts_abi_version() != 3:
         raise RuntimeError("libtilesync_b200.so ABI version mismatch")
     _lib = lib
     return lib

@@ -12,6 +12,8 @@ computes ``A @ W^T``.
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
 from .cusync import CuSync
@@ -44,6 +46,51 @@ class MlpChain:
     def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         self.cs.launch(stream)
         return self.y
+
+    def run_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> torch.Tensor:
+        """End to end from pinned host memory: X row tiles are copied in on one stream,
+        each chunk signalling a row semaphore (ts_stream_signal) that GeMM1's tiles of that
+        row wait on; Y row tiles are copied out on another stream as soon as every GeMM2
+        tile of the row has stored (ts_stream_wait on the row's counter). The paper's
+        tile-level producer -> consumer signalling, with the copy engines as producer
+        and consumer, so both PCIe directions overlap the chain."""
+        from . import _lib
+        lib = _lib.load()
+        rows = self.cs.tile_m  # one semaphore per activation-row tile
+        m = self.x.shape[0]
+        chunks = -(-m // rows)
+        if getattr(self, "_in_sem", None) is None:
+            dev = self.x.device
+            self._in_sem = torch.zeros(chunks, dtype=torch.int32, device=dev)
+            self._out_sem = torch.zeros(chunks, dtype=torch.int32, device=dev)
+            self.prod.in_sem, self.cons.out_sem = self._in_sem, self._out_sem
+            self.cs._desc = None
+            self._epoch = 0
+            self._s_in, self._s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        self._epoch += 1
+        per_row = self.cons.grid.y * self.cons.splits  # out_sem increments per row per launch
+        cur = torch.cuda.current_stream(self.x.device)
+        self._s_in.wait_stream(cur)   # the previous launch no longer reads X ...
+        self._s_out.wait_stream(cur)  # ... nor writes Y
+        with torch.cuda.stream(self._s_in):
+            for c in range(chunks):
+                r = slice(c * rows, min(m, (c + 1) * rows))
+                self.x[r].copy_(x_host[r], non_blocking=True)
+                _lib.check(lib.ts_stream_signal(ctypes.c_void_p(self._in_sem[c:].data_ptr()),
+                                                self._epoch,
+                                                ctypes.c_void_p(self._s_in.cuda_stream)))
+        self.cs.set_in_expected(self.prod, self._epoch)
+        self.cs.launch(cur)
+        with torch.cuda.stream(self._s_out):
+            for c in range(chunks):
+                r = slice(c * rows, min(m, (c + 1) * rows))
+                _lib.check(lib.ts_stream_wait(ctypes.c_void_p(self._out_sem[c:].data_ptr()),
+                                              self._epoch * per_row,
+                                              ctypes.c_void_p(self._s_out.cuda_stream)))
+                y_host[r].copy_(self.y[r], non_blocking=True)
+        cur.wait_stream(self._s_in)
+        cur.wait_stream(self._s_out)
+        return y_host
 
 
 def mlp(x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor, policy: SyncPolicy = RowSync(),

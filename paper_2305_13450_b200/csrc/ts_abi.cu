@@ -358,6 +358,9 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.grid_y = st.n / stage_tile_n;
     sp.wide = wide;
     sp.half_n = half_n;
+    sp.in_sem = st.in_sem;
+    sp.in_expected = st.in_expected;
+    sp.out_sem = st.out_sem;
     if (conv) {
       if (splits > 1) return fail(TS_ERR_CONFIG, "stage %d: no split-K convolutions", s);
       sp.conv_h = st.conv_h;
@@ -502,6 +505,36 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     }
   }
   return TS_OK;
+}
+
+using StreamWriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+StreamWriteFn stream_write_fn() {
+  static StreamWriteFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<StreamWriteFn>(p);
+  });
+  return fn;
+}
+
+using StreamWaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+StreamWaitFn stream_wait_fn() {
+  static StreamWaitFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<StreamWaitFn>(p);
+  });
+  return fn;
 }
 
 __global__ void wait_kernel(const int* flags, int n) {
@@ -652,6 +685,25 @@ int ts_wait_kernel_launch(const int* flags, int n, void* stream) {
   wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flags, n);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_fail(e, "wait_kernel launch");
+}
+
+int ts_stream_signal(int* sem, int value, void* stream) {
+  if (sem == nullptr) return fail(TS_ERR_VALUE, "null semaphore");
+  StreamWriteFn fn = stream_write_fn();
+  if (!fn) return fail(TS_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  // default flags: the write is ordered after (and makes visible) the stream's prior work
+  CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(sem),
+                  static_cast<cuuint32_t>(value), CU_STREAM_WRITE_VALUE_DEFAULT);
+  return r == CUDA_SUCCESS ? TS_OK : fail(TS_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+}
+
+int ts_stream_wait(const int* sem, int value, void* stream) {
+  if (sem == nullptr) return fail(TS_ERR_VALUE, "null semaphore");
+  StreamWaitFn fn = stream_wait_fn();
+  if (!fn) return fail(TS_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(sem),
+                  static_cast<cuuint32_t>(value), CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? TS_OK : fail(TS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
 }
 
 int ts_device_sm_count(int* out) {

@@ -97,6 +97,11 @@ struct StageParams {
   // Conv2DTileSync's k // kk map requires (policies.py:161-165). `halo` = producer row
   // tiles on each side a consumer tile's 3x3 window reaches (extra, untraced waits).
   int conv_h, conv_w, conv_cin, conv_subs, halo;
+  // external row gates (ts_stage_desc.in_sem / out_sem): wait in_sem[tx] >= in_expected
+  // before the first A load; add 1 to out_sem[tx] after the tile's stores
+  int* in_sem;
+  int in_expected;
+  int* out_sem;
 };
 
 struct DepParams {
@@ -339,6 +344,9 @@ __device__ __forceinline__ void dot_batch_warp(const StageParams& st, int row0, 
   }
 }
 
+// diagnostic flag bit 12 (no semaphore waits) also skips the external row gates
+__device__ __forceinline__ bool skip_in_gate(const ChainParams& p) { return (p.flags >> 12) & 1; }
+
 struct Tile {
   int g, s, tb, tx, ty, tz;
 };
@@ -559,6 +567,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           cq = act_row % st.conv_w;
           cp = (act_row / st.conv_w) % st.conv_h;
           cn = act_row / (st.conv_w * st.conv_h);
+        }
+        if (st.in_sem != nullptr && !skip_in_gate(p)) {
+          // external gate: the rows of this tile were copied in (ts_stream_signal)
+          sem_wait(p, st.in_sem + t.tx, st.in_expected);
+          ptx::fence_proxy_async_global();
         }
         const bool waits = d >= 0 && !no_wait;
         const int kbpk = waits ? p.dep[d].kb_per_kstep : 1;
@@ -1188,6 +1201,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
                 *dot_count = n;
               }
             }
+          }
+          if (st.out_sem != nullptr) {
+            // the tile's rows (both CTAs of a pair) are stored: let a copy stream read
+            // them (a PCIe agent, hence system scope)
+            __threadfence_system();
+            atomicAdd(st.out_sem + t.tx, 1);
           }
           trace_event(p, tnow, 4, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
         }

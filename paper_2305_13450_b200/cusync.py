@@ -63,6 +63,8 @@ class CuStage:
     cnt: torch.Tensor | None = None
     kind: str = "gemm"  # "gemm", "dot" (attention's fused softmax-dot) or "conv"
     conv: tuple | None = None  # (N, H, W) of a 3x3 "same" convolution stage
+    in_sem: torch.Tensor | None = None   # external row gate on operand A (ts_stream_signal)
+    out_sem: torch.Tensor | None = None  # per-row "tiles stored" counters (ts_stream_wait)
     tile_n: int = 0     # 0 = the chain's tile_n; 512 = double-width CTA-pair tile
 
     @property
@@ -307,6 +309,8 @@ class CuSync:
                 st.kind, _lib.TS_STAGE_GEMM)
             if st.conv is not None:
                 sd.conv_n, sd.conv_h, sd.conv_w = st.conv
+            sd.in_sem = st.in_sem.data_ptr() if st.in_sem is not None else None
+            sd.out_sem = st.out_sem.data_ptr() if st.out_sem is not None else None
             sd.tile_n = st.tile_n
             sd.workspace = st.ws.data_ptr() if st.ws is not None else None
             sd.counters = st.cnt.data_ptr() if st.cnt is not None else None
@@ -362,6 +366,15 @@ class CuSync:
                                                ctypes.c_void_p(s.cuda_stream)))
 
     __call__ = launch
+
+    def set_in_expected(self, stage: CuStage, value: int) -> None:
+        """Gate value for `stage`'s external row semaphores on the next launch."""
+        if self._desc is None:
+            self._desc = self._build()
+            if self._trace is not None:
+                self._desc.trace = self._trace.data_ptr()
+                self._desc.trace_cap = self._trace_cap
+        self._desc.stages[stage.index].in_expected = value
 
     # -- results -------------------------------------------------------------------------
     def watchdog_fired(self) -> bool:

@@ -438,3 +438,24 @@ def test_normal_split_trace_parity(pol):
     assert sum(1 for e in evs if e.kind == "post") == g1[0] * g1[1] * g1[2]
     _, y_ref = oracle_mlp(x, w1, w2, torch.float16)
     check_close(ch.y, y_ref, torch.float16)
+
+
+@pytest.mark.parametrize("mode,pt,swap", [("fused", 512, False), ("stream", 0, False),
+                                          ("fused", 0, True)])
+def test_run_host_overlapped_copies(mode, pt, swap):
+    """End to end from pinned host memory with row-tile semaphores between the copy
+    engines and the chain (ts_stream_signal / ts_stream_wait): repeated steps give the
+    oracle's result every time."""
+    x, w1, w2 = make(600 if not swap else 40, 768, 1024, 1024, seed=21)
+    kw = dict(swap_ab=True, tile_n=64, prod_splits=3) if swap else \
+        dict(tile_n=256, cta_group=2, prod_tile_n=pt, cons_tile_n=pt)
+    ch = ts.MlpChain(torch.empty_like(x).cuda(), w1.cuda(), w2.cuda(), mode=mode, **kw)
+    xh = x.pin_memory()
+    yh = torch.empty(x.shape[0], w2.shape[0], dtype=x.dtype).pin_memory()
+    _, y_ref = oracle_mlp(x, w1, w2, torch.float16)
+    for _ in range(3):
+        yh.zero_()
+        ch.run_host(xh, yh)
+        torch.cuda.synchronize()
+        assert not ch.cs.watchdog_fired()
+        check_close(yh, y_ref, torch.float16)
