@@ -583,9 +583,23 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         // has no k-step ordering to respect (no dependency, or a single wait at k-step 0).
         const bool ordered = waits && !(p.dep[d].policy == kRow || p.dep[d].policy == kStrided);
         const int rot = (ordered || conv || (p.flags >> 14) & 1) ? 0 : (t.ty * 37 + 5) % k_per;
-        if (waits && rot != 0) {
-          // every wait of the slice (only k-step 0 waits for Row/Strided) before any load
+        // Deep "+R": a Row/Strided consumer waits once (k-step 0) before any activation
+        // load, so it issues the weight boxes of as many K-blocks as the ring holds first,
+        // then waits, then issues their activation boxes — the weights stream while the
+        // producer rows finish (flag bit 21 disables it).
+        const int cap = C::kChunked ? (wide ? C::kBChunks / 2 : (C::kAChunks < C::kBChunks ? C::kAChunks : C::kBChunks))
+                                    : R;
+        const bool deep = waits && !ordered && !conv && reorder && !((p.flags >> 21) & 1);
+        const int pre = deep ? (k_per < cap ? k_per : cap) : 0;
+        const int ea_start = ea;
+        const uint32_t kq_start = kq;
+        auto all_waits = [&]() {
+          // every wait of the slice (only k-step 0 waits for Row/Strided)
           for (int ks = 0; ks * kbpk < st.k_blocks; ++ks) wait_kstep(ks);
+        };
+        if (deep) {
+        } else if (waits && rot != 0) {
+          all_waits();  // before any load
         } else if (waits) {
           // A split-K slice of a consumer still performs every k-step's wait of the
           // reference model (each z-slice of a tile runs all k-steps, engine.py:469-514):
@@ -651,8 +665,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             }
           };
           if (reorder) load_b();
-          if (waits && rot == 0 && kb % kbpk == 0) wait_kstep(kb / kbpk);
-          if (skip_act) {
+          if (!deep && waits && rot == 0 && kb % kbpk == 0) wait_kstep(kb / kbpk);
+          if (skip_act || i < pre) {  // deep "+R": activations of the first `pre` later
           } else if (conv) {
             // im2col box: 128 consecutive output pixels' inputs at filter tap (r, s), 64
             // channels from c0; the map's bounding box starts at (-1, -1), so pixel (p, q)
@@ -676,9 +690,25 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             gi = 0;
           }
           if (++kb == kb_end) kb = kb_begin;
+          if (i + 1 == pre) {
+            // the ring holds the weights of K-blocks [0, pre): wait, then their activations
+            all_waits();
+            for (int j = 0; j < pre && !skip_act; ++j) {
+              const int ej = (ea_start + j) % (C::kChunked ? C::kAChunks : R);
+              const int kbj = kb_begin + (rot + j) % k_per;
+              uint64_t* fbj = &full[(kq_start + j) % kFullRing];
+              uint8_t* dst = C::kChunked ? smem + ej * C::kChunkBytes
+                                         : (SW ? sB + ej * C::kBBytes : sA + ej * C::kABytes);
+              if constexpr (CG == 2) {
+                ptx::tma_load_2d_pair(dst, &st.tmap_a, ptx::mapa(fbj, 0), kbj * kBK, act_row, pol_a);
+              } else {
+                ptx::tma_load_2d(dst, &st.tmap_a, fbj, kbj * kBK, act_row, pol_a);
+              }
+            }
+          }
         }
         // ... and the ones after it once its loads are issued.
-        if (waits && rot == 0)
+        if (waits && rot == 0 && !deep)
           for (int ks = (kb_end + kbpk - 1) / kbpk; ks * kbpk < st.k_blocks; ++ks) wait_kstep(ks);
       }
     }
