@@ -302,6 +302,17 @@ def main():
 
     us_e2e = time_steps(step_e2e, args.steps, args.warmup, torch, dist if use_dist else None)
 
+    def step_e2e_stream():
+        # the same end-to-end step synchronized by stream order: H2D, chain, D2H
+        e2e_chain.x.copy_(xh, non_blocking=True)
+        y = e2e_chain()
+        if use_dist:
+            dist.all_reduce(y)
+        yh.copy_(y, non_blocking=True)
+
+    us_e2e_stream = time_steps(step_e2e_stream, args.steps, args.warmup, torch,
+                               dist if use_dist else None)
+
     sweep = None
     if rank == 0 and world == 1 and not args.no_sweep:
         sweep = {"gpt3_mlp": planner.sweep_mlp(batches=(1, 64, 256, 512, 1024, 2048), device=dev),
@@ -338,7 +349,11 @@ def main():
                      "algorithmic_flops": flops},
         "cpu_baseline": cpu_baseline,
         "e2e": {"value": us_e2e, "unit": "us", "h2d_bytes_per_step": b * H * 2,
-                "d2h_bytes_per_step": b * H * 2},
+                "d2h_bytes_per_step": b * H * 2,
+                "how": "MlpChain.run_host: row-tile H2D chunks signal row semaphores the "
+                       "GeMM1 tiles wait on; Y row tiles leave as soon as their GeMM2 tiles "
+                       "posted (copy engines and kernel synchronized per tile)",
+                "stream_sync_us": us_e2e_stream},
         "gpu_launches": args.steps,
         "clocks": sampler.summary(),
         "candidates": {"fused": cands, "stream": bcands},

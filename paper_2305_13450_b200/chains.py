@@ -192,7 +192,8 @@ class ConvChain:
                  policy: SyncPolicy | None = None, mode: str = "fused", tile_n: int = 128,
                  cta_group: int = 1, keep_sems: bool = False, num_ctas: int = 0,
                  extra_flags: int = 0, prod_order: TileOrder = RowMajor(),
-                 cons_order: TileOrder = RowMajor(), act: str = "relu"):
+                 cons_order: TileOrder = RowMajor(), act: str = "relu", prod_splits: int = 1,
+                 cons_splits: int = 1):
         from .policies import Conv2DTileSync
         n, h, w, _ = x.shape
         self.x, self.w1, self.w2 = x, w1, w2
@@ -200,8 +201,10 @@ class ConvChain:
         self.y = torch.empty(n, h, w, w2.shape[0], dtype=x.dtype, device=x.device)
         self.cs = CuSync(tile_n=tile_n, mode=mode, keep_sems=keep_sems, num_ctas=num_ctas,
                          cta_group=cta_group, extra_flags=extra_flags)
-        self.prod = self.cs.stage_conv(x, w1, self.h, epilogue=act, order=prod_order, id="conv1")
-        self.cons = self.cs.stage_conv(self.h, w2, self.y, order=cons_order, id="conv2")
+        self.prod = self.cs.stage_conv(x, w1, self.h, epilogue=act, order=prod_order, id="conv1",
+                                       splits=prod_splits)
+        self.cons = self.cs.stage_conv(self.h, w2, self.y, order=cons_order, id="conv2",
+                                       splits=cons_splits)
         self.dep = self.cs.dependency(policy or Conv2DTileSync(9), self.prod, self.cons,
                                       operand="a")
 

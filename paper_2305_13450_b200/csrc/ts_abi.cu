@@ -362,7 +362,6 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.in_expected = st.in_expected;
     sp.out_sem = st.out_sem;
     if (conv) {
-      if (splits > 1) return fail(TS_ERR_CONFIG, "stage %d: no split-K convolutions", s);
       sp.conv_h = st.conv_h;
       sp.conv_w = st.conv_w;
       sp.conv_cin = st.k / 9;

@@ -226,7 +226,7 @@ class CuSync:
 
     def stage_conv(self, x: torch.Tensor, w: torch.Tensor, out: torch.Tensor,
                    epilogue: str = "none", order: TileOrder = RowMajor(), id: str | None = None,
-                   tile_n: int = 0) -> CuStage:
+                   tile_n: int = 0, splits: int = 1) -> CuStage:
         """A 3x3, stride-1, padding-1 Conv2D as an implicit GeMM (the paper's ResNet conv
         pairs, PAPER.md:186-204): ``x`` NHWC [N, H, W, Cin], ``w`` KRSC [Cout, 3, 3, Cin],
         ``out`` NHWC [N, H, W, Cout]. Output rows are the N*H*W pixels, columns the output
@@ -246,10 +246,17 @@ class CuSync:
             raise ValueError(f"shape mismatch: x {tuple(x.shape)} w {tuple(w.shape)} "
                              f"out {tuple(out.shape)}")
         self._check_tile_n(tile_n)
+        if splits < 1 or (9 * cin // BK) % splits:
+            raise ConfigError(f"splits={splits} must divide the {9 * cin // BK} K-blocks")
         st = CuStage(self, len(self.stages), id or f"conv{len(self.stages) + 1}",
                      x.view(n * h * wd, cin), w.reshape(w.shape[0], 9 * cin),
-                     out.view(n * h * wd, w.shape[0]), epilogue, order, kind="conv",
-                     conv=(n, h, wd), tile_n=tile_n)
+                     out.view(n * h * wd, w.shape[0]), epilogue, order, splits=splits,
+                     kind="conv", conv=(n, h, wd), tile_n=tile_n)
+        if splits > 1:
+            tiles = st.grid.x * st.grid.y
+            st.ws = torch.empty(tiles * splits * self.tile_m * st.width, dtype=torch.float32,
+                                device=x.device)
+            st.cnt = torch.zeros(tiles * self.cta_group, dtype=torch.int32, device=x.device)
         self.stages.append(st)
         self.device = x.device
         self._desc = None

@@ -164,14 +164,19 @@ def wave_table(m: int, n1: int, n2: int, tile_m: int, tile_n: int, sms: int = 14
 RESNET38_LAYERS = ((56, 64), (28, 128), (14, 256), (7, 512))
 
 
-def conv_candidates(c: int, mode: str):
-    """Tile configurations for a conv pair with `c` channels (output channels = tile
-    columns: a tile no wider than the layer)."""
+def conv_candidates(c: int, mode: str, m: int = 1 << 30):
+    """Tile configurations for a conv pair with `c` channels and `m` output pixels (output
+    channels = tile columns: a tile no wider than the layer). Few pixels (deep layers at
+    small batch) leave most SMs idle, so those also try split-K (reference z slices)."""
     out = []
     for cg, tn in ((1, 64), (1, 128), (2, 128), (1, 256), (2, 256)):
         if tn > c:
             continue
-        out.append(dict(mode=mode, tile_n=tn, cta_group=cg))
+        tiles = -(-m // (128 * cg)) * (c // tn)
+        for z in (1, 2, 4, 8):
+            if z > 1 and (tiles * z > 2 * 148 or (9 * c // 64) % z):
+                continue
+            out.append(dict(mode=mode, tile_n=tn, cta_group=cg, prod_splits=z, cons_splits=z))
     return out
 
 
@@ -191,7 +196,7 @@ def sweep_conv(batches=(1, 8, 32, 128, 256), layers=RESNET38_LAYERS, device=None
             x = torch.randn(b, hw, hw, c, device=device).to(dtype)
             best = {}
             for mode in ("fused", "stream"):
-                for kw in conv_candidates(c, mode):
+                for kw in conv_candidates(c, mode, b * hw * hw):
                     ch = ConvChain(x, w1, w2, **kw)
                     us = _time(ch, iters=20)
                     if ch.cs.watchdog_fired():

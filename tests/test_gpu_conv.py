@@ -34,8 +34,10 @@ def check_close(dev, ref, dtype):
 
 
 CASES = [
-    # n, h, w, c, tile_n, cta_group, mode
+    # n, h, w, c, tile_n, cta_group, mode[, splits]
     (1, 56, 56, 64, 64, 1, "fused"),     # ResNet-38 layer 1
+    (1, 7, 7, 512, 128, 1, "fused", 4),  # layer 4 at batch 1: split-K slices
+    (2, 14, 14, 256, 256, 2, "fused", 2),
     (2, 28, 28, 128, 128, 1, "fused"),   # layer 2
     (4, 14, 14, 256, 128, 2, "fused"),   # layer 3
     (8, 7, 7, 512, 256, 2, "fused"),     # layer 4
@@ -44,11 +46,14 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("n,h,w,c,tn,cg,mode", CASES)
+@pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
-def test_conv_pair_numerics(n, h, w, c, tn, cg, mode, dtype):
+def test_conv_pair_numerics(case, dtype):
+    n, h, w, c, tn, cg, mode = case[:7]
+    z = case[7] if len(case) > 7 else 1
     x, w1, w2 = make(n, h, w, c, dtype)
-    ch = ts.ConvChain(x.cuda(), w1.cuda(), w2.cuda(), mode=mode, tile_n=tn, cta_group=cg)
+    ch = ts.ConvChain(x.cuda(), w1.cuda(), w2.cuda(), mode=mode, tile_n=tn, cta_group=cg,
+                      prod_splits=z, cons_splits=z)
     for _ in range(3):
         y = ch()
     torch.cuda.synchronize()
