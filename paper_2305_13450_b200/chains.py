@@ -151,7 +151,7 @@ class AttentionChain:
                  second_policy: SyncPolicy | None = None, mode: str = "fused",
                  cta_group: int = 2, keep_sems: bool = False, num_ctas: int = 0,
                  extra_flags: int = 0, tile_n: int = 256, qkv_splits: int = 1,
-                 out_splits: int = 1):
+                 out_splits: int = 1, out_tile_n: int = 0):
         """``qkv_splits`` / ``out_splits`` > 1 split the GeMMs' K into reference z-slices
         (each posts once; StridedSync/TileSync expect x z) — the QKV GeMM of a short
         sequence has too few output tiles to fill 148 SMs otherwise."""
@@ -171,7 +171,8 @@ class AttentionChain:
         self.s_qkv = self.cs.stage(x, w_qkv, self.qkv, order=StridedRowMajor(stride), id="qkv",
                                    splits=qkv_splits)
         self.s_dot = self.cs.stage_dot(self.qkv, self.dot, id="dot")
-        self.s_out = self.cs.stage(self.dot, w2, self.y, id="out", splits=out_splits)
+        self.s_out = self.cs.stage(self.dot, w2, self.y, id="out", splits=out_splits,
+                                   tile_n=out_tile_n)
         self.cs.dependency(StridedSync(stride), self.s_qkv, self.s_dot, operand="qkv")
         self.cs.dependency(second_policy or TileSync(), self.s_dot, self.s_out, operand="a")
 

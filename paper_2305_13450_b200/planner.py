@@ -132,14 +132,16 @@ def sweep_attention(seqs=(512, 1024, 2048), hidden=12288, heads=12, device=None)
         x = torch.randn(s, hidden, device=device).half()
         best = {}
         for mode in ("fused", "stream"):
-            for cg, z in itertools.product((1, 2), (1, 2, 4)):
+            for cg, z, ow in itertools.product((1, 2), (1, 2, 4), (0, 512)):
+                if ow and cg == 1:
+                    continue  # double-width output tiles are CTA-pair tiles
                 for pol in ([RowSync(), TileSync()] if mode == "fused" else [TileSync()]):
                     ch = AttentionChain(x, wqkv, w2, second_policy=pol, mode=mode, cta_group=cg,
-                                        qkv_splits=z)
+                                        qkv_splits=z, out_tile_n=ow)
                     us = _time(ch, iters=20)
                     if us < best.get(mode, (float("inf"),))[0]:
                         best[mode] = (us, {"cta_group": cg, "policy": type(pol).__name__,
-                                           "qkv_splits": z})
+                                           "qkv_splits": z, "out_tile_n": ow or 256})
         cu = _time(lambda: _torch_attention(x, wqkv, w2, heads), iters=20)
         flops = 2 * s * hidden * 3 * heads * 128 + 2 * s * heads * 128 * hidden
         rows.append({"seq": s, "fused_us": best["fused"][0], "stream_us": best["stream"][0],

@@ -267,17 +267,22 @@ def test_split_trace_counts_follow_reference_z(pol, z1, z2):
                                                  (128, 4, 1, "fused", 256, 1),
                                                  (200, 4, 2, "fused", 128, 1),
                                                  (256, 2, 2, "fused", 256, 4),
-                                                 (300, 3, 1, "fused", 128, 2)])
+                                                 (300, 3, 1, "fused", 128, 2),
+                                                 (520, 2, 2, "fused", 256, 512)])
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
 def test_attention_chain(m, heads, cg, mode, tn, z, dtype):
-    """QKV (StridedRowMajor) -> fused dot (StridedSync) -> out GeMM (TileSync)."""
+    """QKV (StridedRowMajor) -> fused dot (StridedSync) -> out GeMM (TileSync).
+    z = 512 encodes a double-width output stage instead of QKV split-K slices."""
+    ow = 512 if z == 512 else 0
+    z = 1 if z == 512 else z
     g = torch.Generator().manual_seed(11)
     h = 512
     x = torch.randn(m, h, generator=g).to(dtype)
     wqkv = (torch.randn(3 * heads * 128, h, generator=g) / h ** 0.5).to(dtype)
     w2 = (torch.randn(h, heads * 128, generator=g) / (heads * 128) ** 0.5).to(dtype)
     ch = ts.AttentionChain(x.cuda(), wqkv.cuda(), w2.cuda(), mode=mode, cta_group=cg,
-                           keep_sems=(mode == "fused"), tile_n=tn, qkv_splits=z)
+                           keep_sems=(mode == "fused"), tile_n=tn, qkv_splits=z,
+                           out_tile_n=ow)
     ch.cs.enable_trace()
     ch()
     torch.cuda.synchronize()
