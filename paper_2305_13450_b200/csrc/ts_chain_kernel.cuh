@@ -434,6 +434,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       ptx::tma_prefetch_desc(&p.st[s].tmap_b);
     }
   }
+  __syncthreads();  // barrier init (thread 0) before the allocator warp writes tmem_slot
   if (warp == 2) ptx::tmem_alloc<C::kTmemCols, CG>(tmem_slot);
   ptx::tc_fence_before();
   if constexpr (CG == 2) {
