@@ -1061,6 +1061,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         }
         __threadfence();
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        if (threadIdx.x == 128 && leader && p.trace != nullptr)  // partials written (ext.)
+          trace_event(p, ptx::global_timer(), 9, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
         if (threadIdx.x == 128) {
           const int half_id = tile_id * CG + static_cast<int>(rank);
           const int old = atomicAdd(&st.cnt[half_id], 1);

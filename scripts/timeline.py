@@ -77,6 +77,14 @@ def summarize(cs, label):
                   f"accumulator ready {sum(lag) / len(lag) / 1e3:.1f} us)")
         elif d:
             print(f"  {st.id}: compute mean {sum(d) / len(d) / 1e3:.1f} us")
+    pw = {(r.stage, r.tb): r.t_ns for r in recs if r.kind == 9}
+    for s_i, st in enumerate(cs.stages):
+        w = [pw[k] - eb[k] for k in pw if k[0] == s_i and k in eb]
+        rest = [ee[k] - pw[k] for k in pw if k[0] == s_i and k in ee]
+        if w:
+            print(f"  {st.id}: split-K partial write mean {sum(w) / len(w) / 1e3:.1f} us, "
+                  f"then count + reduce mean {sum(rest) / len(rest) / 1e3:.1f} us "
+                  f"(max {max(rest) / 1e3:.1f})")
     # MMA idle per CTA(-pair leader): before its first tile, between tiles, after its last
     per_sm = defaultdict(list)
     for k, r in me.items():
