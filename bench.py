@@ -317,7 +317,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_sweep:
         sweep = {"gpt3_mlp": planner.sweep_mlp(batches=(1, 64, 256, 512, 1024, 2048), device=dev),
                  "gpt3_attention": planner.sweep_attention(device=dev),
-                 "resnet38_conv_pairs": planner.sweep_conv(batches=(1, 8, 32), device=dev)}
+                 "resnet38_conv_pairs": planner.sweep_conv(batches=(1, 8, 32), device=dev),
+                 "llama8b_swiglu": planner.sweep_swiglu(device=dev)}
 
     if rank != 0:
         if use_dist:

@@ -219,3 +219,49 @@ def sweep_conv(batches=(1, 8, 32, 128, 256), layers=RESNET38_LAYERS, device=None
                          "fused": {k: v for k, v in best["fused"][1].items() if k != "mode"},
                          "stream": {k: v for k, v in best["stream"][1].items() if k != "mode"}})
     return rows
+
+
+def sweep_swiglu(batches=(256, 1024, 2048), tps=(8, 1), hidden=4096, ffn=14336, device=None):
+    """LLaMA-style 8B SwiGLU MLP (BASELINE.json configs[3]), bf16, the per-rank chain of a
+    TP=tp shard: H = SiLU(X Wg^T) * (X Wu^T) (gate/up interleaved per tile), Y = H Wd^T.
+    Best fused vs best stream-synchronized configuration vs torch/cuBLAS."""
+    from .chains import SwigluChain, interleave_gate_up
+    torch.manual_seed(9)
+    rows = []
+    for tp in tps:
+        f = ffn // tp
+        wg = (torch.randn(f, hidden, device=device) / hidden ** 0.5).bfloat16()
+        wu = (torch.randn(f, hidden, device=device) / hidden ** 0.5).bfloat16()
+        wd = (torch.randn(hidden, f, device=device) / f ** 0.5).bfloat16()
+        packed = {w: interleave_gate_up(wg, wu, w) for w in (256, 512)}
+        for b in batches:
+            x = torch.randn(b, hidden, device=device).bfloat16()
+            best = {}
+            for mode in ("fused", "stream"):
+                pols = [RowSync(), TileSync()] if mode == "fused" else [RowSync()]
+                for pw, cw, pol in itertools.product((256, 512), (0, 512), pols):
+                    if (f // 2) % (pw // 2) or f % pw // 2:
+                        continue
+                    try:
+                        ch = SwigluChain(x, packed[pw], wd, policy=pol, mode=mode, tile_n=256,
+                                         cta_group=2, prod_tile_n=pw if pw == 512 else 0,
+                                         cons_tile_n=cw)
+                    except Exception:  # shapes a width does not divide
+                        continue
+                    us = _time(ch, iters=20)
+                    if ch.cs.watchdog_fired():
+                        continue
+                    if us < best.get(mode, (float("inf"),))[0]:
+                        best[mode] = (us, {"policy": type(pol).__name__,
+                                           "tile": f"256x{pw}/256x{cw or 256}"})
+
+            def torch_mlp():
+                return (torch.nn.functional.silu(x @ wg.t()) * (x @ wu.t())) @ wd.t()
+            cu = _time(torch_mlp, iters=20)
+            flops = 2 * b * hidden * f * 3
+            fu, su = best["fused"][0], best["stream"][0]
+            rows.append({"tp": tp, "batch": b, "ffn_shard": f, "fused_us": fu, "stream_us": su,
+                         "cublas_us": cu, "speedup_vs_stream": su / fu,
+                         "speedup_vs_cublas": cu / fu, "fused_tflops": flops / fu / 1e6,
+                         "fused": best["fused"][1], "stream": best["stream"][1]})
+    return rows
