@@ -143,7 +143,7 @@ struct Cfg {
   static constexpr int kThreads = 128 + kEpiThreads;
   static constexpr int kChunkBytes = 16384;
   // A boxes and B boxes live in separate chunk rings (A ring first in smem)
-  static constexpr int kAChunks = 6;
+  static constexpr int kAChunks = 4;
   static constexpr int kBChunks = 8;
   static constexpr int kChunks = kAChunks + kBChunks;
   static constexpr int kTileM = SW ? BN : 128 * CG;  // activation rows of a tile
@@ -162,7 +162,12 @@ struct Cfg {
   static constexpr int kAccCols = kAcc * BN;           // TMEM columns of one tile buffer
   static constexpr int kTmemCols = 2 * kAccCols;       // two tile buffers
   static constexpr int kRing = kChunked ? kChunks : kStages;  // ring entries
-  static constexpr int kBarOffset = kChunked ? kChunks * kChunkBytes : kStages * kStageBytes;
+  // chunked tiles: a 4-KB per-warp staging block after the ring turns the epilogue's
+  // row-per-lane stores into 512-B coalesced ones (st.global from row-per-lane registers
+  // touches 32 lines per instruction: measured ~25 GB/s per SM)
+  static constexpr int kStageOff = kChunked ? kChunks * kChunkBytes : 0;
+  static constexpr int kBarOffset =
+      kChunked ? kStageOff + (kEpiThreads / 32) * 4096 : kStages * kStageBytes;
   // K-block full, commit-group empty; tmem full/empty x2; tile ring full/empty; peer_done
   static constexpr int kNumBars = kFullRing + kCommitRing + 4 + 2 * kTileRing + kPeerRing;
   // + tile ring ids, TMEM slot, flags and the last-arriver dot list (64 ints), ring-entry
@@ -255,7 +260,7 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
 // the semaphores stay monotone as in SemaphoreArray, policies.py:84-99). Exponential
 // back-off keeps the polling traffic and issue slots of waiting SMs low.
 __device__ __forceinline__ void sem_wait(const ChainParams& p, const int* sem, int expected) {
-  // Relaxed probes, then one acquire fence once the count is reached (an acquiring load
+  // Relaxed probes, then one acquiring load once the count is reached (an acquiring load
   // per probe would invalidate L1 on every iteration).
   if (ptx::ld_relaxed_gpu(sem) < expected) {
     const bool watchdog = (p.flags & TS_FLAG_NO_WATCHDOG) == 0;
@@ -271,7 +276,9 @@ __device__ __forceinline__ void sem_wait(const ChainParams& p, const int* sem, i
       }
     }
   }
-  ptx::fence_acq_rel_gpu();
+  // acquire: synchronizes-with the producer's release post (cheaper than a full
+  // fence.acq_rel, which also orders this thread's outstanding accesses)
+  (void)ptx::ld_acquire_gpu(sem);
 }
 
 template <typename T>
@@ -429,7 +436,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
   }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.n_stages; ++s) {
-      if (p.st[s].kind != kStageGemm) continue;  // pointwise stages have no tensor maps
+      if (p.st[s].kind == kStageDot) continue;  // the pointwise stage has no tensor maps
       ptx::tma_prefetch_desc(&p.st[s].tmap_a);
       ptx::tma_prefetch_desc(&p.st[s].tmap_b);
     }
@@ -839,6 +846,26 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
     // ===================== epilogue =====================
     const int ew = warp & 3;         // TMEM lanes [32*ew, 32*ew+32) (a warp's lane quarter)
     const int eg = (warp - 4) >> 2;  // column group (chunked tiles: 0 or 1)
+    // Coalesced row stores through this warp's staging block: every lane holds 128 B of
+    // its row (32 words); they go to shared memory (16-B granules XOR-swizzled by row)
+    // and come back as 4 rows x 128 B per instruction, written with 16-B stores to
+    // dst(row_in_warp, granule) (nullptr = skip).
+    uint32_t* stg = reinterpret_cast<uint32_t*>(smem + C::kStageOff + (warp - 4) * 4096);
+    auto stage_rows = [&](const uint32_t (&v)[32], auto&& dst) {
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+        *reinterpret_cast<uint4*>(stg + lane * 32 + ((g ^ (lane & 7)) * 4)) =
+            make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = 4 * i + (lane >> 3), g = lane & 7;
+        const uint4 q = *reinterpret_cast<const uint4*>(stg + rr * 32 + ((g ^ (rr & 7)) * 4));
+        uint4* d = dst(rr, g);
+        if (d != nullptr) *d = q;
+      }
+      __syncwarp();
+    };
     uint32_t local = 0;  // GeMM tiles (peer_done parity)
     uint32_t u = 0;      // TMEM accumulator-slot uses, as counted by the MMA warp
     uint32_t tmem_empty_remote[2] = {0, 0};
@@ -1053,9 +1080,17 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             uint32_t r[32];
             ptx::tmem_ld_32x32b_x32(tcol(x), r);
             ptx::tmem_ld_wait();
-            float* dst = mine + (static_cast<size_t>(x / 32) * 128 + rl_row) * 32;
+            if constexpr (C::kChunked) {
+              // plane rows of this warp are 32 consecutive 128-B rows of chunk x / 32
+              float* wbase = mine + (static_cast<size_t>(x / 32) * 128 + ew * 32) * 32;
+              stage_rows(r, [&](int rr, int g) {
+                return reinterpret_cast<uint4*>(wbase + rr * 32 + g * 4);
+              });
+            } else {
+              float* dst = mine + (static_cast<size_t>(x / 32) * 128 + rl_row) * 32;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) ptx::st_global_v8(dst + 8 * q, r + 8 * q);
+              for (int q = 0; q < 4; ++q) ptx::st_global_v8(dst + 8 * q, r + 8 * q);
+            }
           }
           release_slot(j);
         }
