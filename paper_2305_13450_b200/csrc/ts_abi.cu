@@ -367,6 +367,9 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       sp.conv_cin = st.k / 9;
       sp.conv_subs = 1;  // K channel tile = 64 unless a producer's column tile sets it
       sp.halo = (st.conv_w + 1 + tile_m - 1) / tile_m;
+      if (sp.halo > 2)
+        return fail(TS_ERR_CONFIG, "stage %d: image width %d needs a 3x3 halo of %d row tiles "
+                    "(at most 2; use larger tiles)", s, st.conv_w, sp.halo);
     }
     sp.splits = splits;
     sp.ws = st.workspace;

@@ -259,26 +259,48 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
 // Spin until sem >= expected (the paper's wait_till, relaxed to >= so
 // the semaphores stay monotone as in SemaphoreArray, policies.py:84-99). Exponential
 // back-off keeps the polling traffic and issue slots of waiting SMs low.
-__device__ __forceinline__ void sem_wait(const ChainParams& p, const int* sem, int expected) {
-  // Relaxed probes, then one acquiring load once the count is reached (an acquiring load
-  // per probe would invalidate L1 on every iteration).
-  if (ptx::ld_relaxed_gpu(sem) < expected) {
-    const bool watchdog = (p.flags & TS_FLAG_NO_WATCHDOG) == 0;
-    uint64_t t0 = ptx::global_timer();
-    uint32_t ns = 32;
+__device__ __forceinline__ void sem_spin(const ChainParams& p, const int* sem, int expected) {
+  // relaxed probes with back-off (an acquiring load per probe would invalidate L1 on
+  // every iteration), then one acquiring load
+  const bool watchdog = (p.flags & TS_FLAG_NO_WATCHDOG) == 0;
+  uint64_t t0 = ptx::global_timer();
+  uint32_t ns = 32;
 #pragma unroll 1
-    while (ptx::ld_relaxed_gpu(sem) < expected) {
-      __nanosleep(ns);
-      if (ns < 256) ns <<= 1;
-      if (watchdog && ptx::global_timer() - t0 > kWatchdogNs) {
-        atomicExch(&p.scratch[3], 1);
-        break;
-      }
+  while (ptx::ld_relaxed_gpu(sem) < expected) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+    if (watchdog && ptx::global_timer() - t0 > kWatchdogNs) {
+      atomicExch(&p.scratch[3], 1);
+      break;
     }
   }
-  // acquire: synchronizes-with the producer's release post (cheaper than a full
-  // fence.acq_rel, which also orders this thread's outstanding accesses)
   (void)ptx::ld_acquire_gpu(sem);
+}
+
+// Block until *s0 >= e0 and, for the optional extra semaphores (nullptr = none), *si >=
+// ei. The first probes are acquiring loads issued back to back, so a satisfied wait
+// costs one L2 round trip in the producer lane's critical path (two serialized loads
+// per semaphore starved the MMA warp on short tiles). No arrays: they would live in
+// local memory.
+__device__ __forceinline__ void sem_wait5(const ChainParams& p, const int* s0, int e0,
+                                          const int* s1 = nullptr, int e1 = 0,
+                                          const int* s2 = nullptr, int e2 = 0,
+                                          const int* s3 = nullptr, int e3 = 0,
+                                          const int* s4 = nullptr, int e4 = 0) {
+  const int v0 = ptx::ld_acquire_gpu(s0);
+  const int v1 = s1 ? ptx::ld_acquire_gpu(s1) : 0;
+  const int v2 = s2 ? ptx::ld_acquire_gpu(s2) : 0;
+  const int v3 = s3 ? ptx::ld_acquire_gpu(s3) : 0;
+  const int v4 = s4 ? ptx::ld_acquire_gpu(s4) : 0;
+  if (v0 < e0) sem_spin(p, s0, e0);
+  if (s1 && v1 < e1) sem_spin(p, s1, e1);
+  if (s2 && v2 < e2) sem_spin(p, s2, e2);
+  if (s3 && v3 < e3) sem_spin(p, s3, e3);
+  if (s4 && v4 < e4) sem_spin(p, s4, e4);
+}
+
+__device__ __forceinline__ void sem_wait(const ChainParams& p, const int* sem, int expected) {
+  sem_wait5(p, sem, expected);
 }
 
 template <typename T>
@@ -553,19 +575,27 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           if (leader)
             trace_event(p, ptx::global_timer(), 1, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
                         t.ty, t.tz);
-          sem_wait(p, dp.sem + w.sem, w.expected);
+          // Halo (extension): a 3x3 window of output rows [m0, m0 + tile_m) reads input
+          // pixels up to W + 1 rows away, i.e. the same k-step's producer tiles of
+          // neighbouring row tiles; the reference map names only row tx. Those waits ride
+          // along untraced (their wait_end is not an event of the reference model).
+          // halo rows tx-2 .. tx+2 (halo <= 2, checked on the host)
+          auto halo_sem = [&](int dx, int& e) -> const int* {
+            const int x = t.tx + dx;
+            if (dx < -st.halo || dx > st.halo || x < 0 || x >= dp.pgx) return nullptr;
+            const Wait h = consumer_wait(dp.policy, dp.param, x, t.ty, ks, pg, dp.pgz);
+            e = h.expected;
+            return h.sem >= 0 ? dp.sem + h.sem : nullptr;
+          };
+          int e1 = 0, e2 = 0, e3 = 0, e4 = 0;
+          const int* h1 = halo_sem(-1, e1);
+          const int* h2 = halo_sem(1, e2);
+          const int* h3 = halo_sem(-2, e3);
+          const int* h4 = halo_sem(2, e4);
+          sem_wait5(p, dp.sem + w.sem, w.expected, h1, e1, h2, e2, h3, e3, h4, e4);
           if (leader)
             trace_event(p, ptx::global_timer(), 2, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
                         t.ty, t.tz);
-          // Halo (extension, untraced): a 3x3 window of output rows [m0, m0 + tile_m)
-          // reads input pixels up to W + 1 rows away, i.e. the same k-step's producer
-          // tiles of neighbouring row tiles. The reference map names only row tx.
-          for (int dx = -st.halo; dx <= st.halo; ++dx) {
-            const int x = t.tx + dx;
-            if (dx == 0 || x < 0 || x >= dp.pgx) continue;
-            Wait h = consumer_wait(dp.policy, dp.param, x, t.ty, ks, pg, dp.pgz);
-            if (h.sem >= 0) sem_wait(p, dp.sem + h.sem, h.expected);
-          }
           ptx::fence_proxy_async_global();
         };
         // conv: the first output pixel of this CTA's rows, as NHW coordinates
@@ -597,7 +627,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         // producer rows finish (flag bit 21 disables it).
         const int cap = C::kChunked ? (wide ? C::kBChunks / 2 : (C::kAChunks < C::kBChunks ? C::kAChunks : C::kBChunks))
                                     : R;
-        const bool deep = waits && !ordered && !conv && reorder && !((p.flags >> 21) & 1);
+        // Ordered policies (Tile, Conv2D) defer the waits of the k-steps inside the first
+        // `pre` K-blocks the same way (their later k-steps wait inline), which hides the
+        // loaded latency of a satisfied wait (~2 us of L2 round trip) behind weight loads.
+        const bool deep = waits && reorder && !((p.flags >> 21) & 1);
         const int pre = deep ? (k_per < cap ? k_per : cap) : 0;
         const int ea_start = ea;
         const uint32_t kq_start = kq;
@@ -605,7 +638,36 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           // every wait of the slice (only k-step 0 waits for Row/Strided)
           for (int ks = 0; ks * kbpk < st.k_blocks; ++ks) wait_kstep(ks);
         };
-        if (deep) {
+        // conv: K-block kb = (channel tile, tap, 64-channel sub-block)
+        // returns (c0 << 4) | tap
+        auto conv_coords = [&](int kb) -> int {
+          const int per_tile = 9 * st.conv_subs;
+          const int rem = kb % per_tile;
+          return ((((kb / per_tile) * st.conv_subs + rem % st.conv_subs) * kBK) << 4) | (rem / st.conv_subs);
+        };
+        // the activation (A) box of K-block kb into `dst`, completing on barrier fb; conv:
+        // cc = conv_coords(kb)
+        auto load_a = [&](uint8_t* dst, uint64_t* fb, int kb, int cc) {
+          const uint32_t fbc = CG == 2 ? ptx::mapa(fb, 0) : 0;
+          if (conv) {
+            // im2col box: 128 consecutive output pixels' inputs at filter tap (r, s), 64
+            // channels from c0; the map's bounding box starts at (-1, -1), so pixel
+            // (p, q) sits at box coordinate (p - 1, q - 1) and the tap adds (r, s);
+            // outside the image the TMA fills zeros (the 3x3 "same" padding).
+            const int c0 = cc >> 4, tap = cc & 15;
+            const uint16_t r = static_cast<uint16_t>(tap / 3), s = static_cast<uint16_t>(tap % 3);
+            if constexpr (CG == 2) {
+              ptx::tma_load_im2col_pair(dst, &st.tmap_a, fbc, c0, cq - 1, cp - 1, cn, s, r, pol_a);
+            } else {
+              ptx::tma_load_im2col(dst, &st.tmap_a, fb, c0, cq - 1, cp - 1, cn, s, r, pol_a);
+            }
+          } else if constexpr (CG == 2) {
+            ptx::tma_load_2d_pair(dst, &st.tmap_a, fbc, kb * kBK, act_row, pol_a);
+          } else {
+            ptx::tma_load_2d(dst, &st.tmap_a, fb, kb * kBK, act_row, pol_a);
+          }
+        };
+        if (deep && !ordered) {
         } else if (waits && rot != 0) {
           all_waits();  // before any load
         } else if (waits) {
@@ -613,6 +675,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           // reference model (each z-slice of a tile runs all k-steps, engine.py:469-514):
           // the ones before its K range up front (they cover the k-step it starts in) ...
           for (int ks = 0; ks * kbpk < kb_begin; ++ks) wait_kstep(ks);
+        }
+        // conv K-block coordinates, advanced without divisions (rot = 0 for conv)
+        int cv_sub = 0, cv_tap = 0, cv_ct = 0;
+        if (conv) {
+          const int per_tile = 9 * st.conv_subs;
+          cv_ct = kb_begin / per_tile;
+          cv_tap = (kb_begin % per_tile) / st.conv_subs;
+          cv_sub = kb_begin % st.conv_subs;
         }
 #pragma unroll 1
         for (int i = 0, kb = kb_begin + rot, gi = 0; i < k_per; ++i) {
@@ -654,13 +724,18 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             w_dst = SW ? sA + e0 * C::kABytes : sB + e0 * C::kBBytes;
           }
           // weight K coordinate; conv: K-block kb = (channel tile, tap, sub-block)
-          int wk = kb * kBK, c0 = 0, tap = 0;
+          int wk = kb * kBK, cc = 0;
           if (conv) {
-            const int per_tile = 9 * st.conv_subs;
-            const int rem = kb % per_tile;
-            tap = rem / st.conv_subs;
-            c0 = ((kb / per_tile) * st.conv_subs + rem % st.conv_subs) * kBK;
-            wk = tap * st.conv_cin + c0;  // KRSC: [tap][cin] inside a weight row
+            const int c0 = (cv_ct * st.conv_subs + cv_sub) * kBK;
+            cc = (c0 << 4) | cv_tap;
+            wk = cv_tap * st.conv_cin + c0;  // KRSC: [tap][cin] inside a weight row
+            if (++cv_sub == st.conv_subs) {
+              cv_sub = 0;
+              if (++cv_tap == 9) {
+                cv_tap = 0;
+                ++cv_ct;
+              }
+            }
           }
           auto load_b = [&]() {
             if constexpr (CG == 2) {
@@ -673,24 +748,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             }
           };
           if (reorder) load_b();
-          if (!deep && waits && rot == 0 && kb % kbpk == 0) wait_kstep(kb / kbpk);
-          if (skip_act || i < pre) {  // deep "+R": activations of the first `pre` later
-          } else if (conv) {
-            // im2col box: 128 consecutive output pixels' inputs at filter tap (r, s), 64
-            // channels from c0; the map's bounding box starts at (-1, -1), so pixel (p, q)
-            // sits at box coordinate (p - 1, q - 1) and the tap adds (r, s); outside the
-            // image the TMA fills zeros (the 3x3 "same" padding).
-            const uint16_t r = static_cast<uint16_t>(tap / 3), s = static_cast<uint16_t>(tap % 3);
-            if constexpr (CG == 2) {
-              ptx::tma_load_im2col_pair(act_dst, &st.tmap_a, fbc, c0, cq - 1, cp - 1, cn, s, r, pol_a);
-            } else {
-              ptx::tma_load_im2col(act_dst, &st.tmap_a, fb, c0, cq - 1, cp - 1, cn, s, r, pol_a);
-            }
-          } else if constexpr (CG == 2) {
-            ptx::tma_load_2d_pair(act_dst, &st.tmap_a, fbc, kb * kBK, act_row, pol_a);
-          } else {
-            ptx::tma_load_2d(act_dst, &st.tmap_a, fb, kb * kBK, act_row, pol_a);
-          }
+          if (i >= pre && waits && rot == 0 && kb % kbpk == 0) wait_kstep(kb / kbpk);
+          if (!skip_act && i >= pre) load_a(act_dst, fb, kb, cc);  // deep "+R": first `pre` later
           if (!reorder) load_b();
           ++kq;
           if (++gi == group || i + 1 == k_per) {  // the K-block closes a commit group
@@ -700,23 +759,25 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           if (++kb == kb_end) kb = kb_begin;
           if (i + 1 == pre) {
             // the ring holds the weights of K-blocks [0, pre): wait, then their activations
-            all_waits();
+            if (!ordered) {
+              all_waits();
+            } else {
+              for (int j = 0; j < pre; ++j) {  // the k-steps starting in [kb_begin, +pre)
+                const int kbj = kb_begin + j;
+                if (kbj % kbpk == 0) wait_kstep(kbj / kbpk);
+              }
+            }
             for (int j = 0; j < pre && !skip_act; ++j) {
               const int ej = (ea_start + j) % (C::kChunked ? C::kAChunks : R);
               const int kbj = kb_begin + (rot + j) % k_per;
-              uint64_t* fbj = &full[(kq_start + j) % kFullRing];
               uint8_t* dst = C::kChunked ? smem + ej * C::kChunkBytes
                                          : (SW ? sB + ej * C::kBBytes : sA + ej * C::kABytes);
-              if constexpr (CG == 2) {
-                ptx::tma_load_2d_pair(dst, &st.tmap_a, ptx::mapa(fbj, 0), kbj * kBK, act_row, pol_a);
-              } else {
-                ptx::tma_load_2d(dst, &st.tmap_a, fbj, kbj * kBK, act_row, pol_a);
-              }
+              load_a(dst, &full[(kq_start + j) % kFullRing], kbj, conv ? conv_coords(kbj) : 0);
             }
           }
         }
         // ... and the ones after it once its loads are issued.
-        if (waits && rot == 0 && !deep)
+        if (waits && rot == 0 && !(deep && !ordered))
           for (int ks = (kb_end + kbpk - 1) / kbpk; ks * kbpk < st.k_blocks; ++ks) wait_kstep(ks);
       }
     }
@@ -1236,7 +1297,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             ptx::mbar_wait_cluster(&peer_done[local % kPeerRing], (local / kPeerRing) & 1);
           const uint64_t tnow = ptx::global_timer();
           if (st.n_out_deps > 0) {
-            __threadfence();
+            // release: the epilogue's stores (ordered before this thread by the named
+            // barrier) become visible before the post; diagnostic flag bit 22 times the
+            // post without the full fence
+            if (!((p.flags >> 22) & 1)) __threadfence();
             ptx::fence_proxy_async_global();
             for (int i = 0; i < st.n_out_deps; ++i) {
               const int d = st.out_deps[i];

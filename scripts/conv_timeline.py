@@ -1,0 +1,25 @@
+"""Device-trace timeline of a ResNet conv pair. argv: N HW C tile_n cg mode [flags z]"""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2305_13450_b200 as ts  # noqa: E402
+from scripts.timeline import summarize  # noqa: E402
+
+n, hw, c, tn, cg = (int(v) for v in sys.argv[1:6])
+mode = sys.argv[6]
+flags = int(sys.argv[7], 0) if len(sys.argv) > 7 else 0
+z = int(sys.argv[8]) if len(sys.argv) > 8 else 1
+x = torch.randn(n, hw, hw, c, device="cuda").half()
+w1 = (torch.randn(c, 3, 3, c, device="cuda") / (9 * c) ** 0.5).half()
+w2 = (torch.randn(c, 3, 3, c, device="cuda") / (9 * c) ** 0.5).half()
+ch = ts.ConvChain(x, w1, w2, mode=mode, tile_n=tn, cta_group=cg, extra_flags=flags,
+                  prod_splits=z, cons_splits=z)
+for _ in range(3):
+    ch()
+ch.cs.enable_trace()
+for _ in range(2):
+    ch()
+torch.cuda.synchronize()
+summarize(ch.cs, f"conv {sys.argv[1:]}")
