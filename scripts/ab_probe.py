@@ -22,9 +22,9 @@ def run(ts, tag):
                   (1024, dict(tile_n=256, cta_group=2, prod_tile_n=512, cons_tile_n=512,
                               cons_order=ts.BandedColumnMajor(4)))):
         x = torch.randn(b, H, device="cuda").half()
-        for mode in ("fused", "stream"):
-            ch = ts.MlpChain(x, w1, w2, policy=ts.RowSync(), mode=mode, **kw)
-            out.append((f"mlp B={b} {mode}", time_fn(ch, iters=50)))
+        for mode, pol in (("fused", ts.RowSync()), ("fused", ts.TileSync()), ("stream", ts.RowSync())):
+            ch = ts.MlpChain(x, w1, w2, policy=pol, mode=mode, **kw)
+            out.append((f"mlp B={b} {mode} {type(pol).__name__}", time_fn(ch, iters=50)))
     for n, hw, c, tn in ((32, 56, 64, 64), (8, 28, 128, 128)):
         x = torch.randn(n, hw, hw, c, device="cuda").half()
         wc = (torch.randn(c, 3, 3, c, device="cuda") / (9 * c) ** 0.5).half()
