@@ -181,6 +181,59 @@ def main() -> None:
                        "deps": [dep_dict(d) for d in sc.deps], "mode": sc.mode.value,
                        "cases": cases})
     (OUT / "traces.json").write_text(json.dumps(traces, separators=(",", ":")))
+
+    # ---------------- engine layer (engine.py:134-217) ----------------
+    eng = {"gates": [], "kstep": [], "errors": []}
+    gate_scen = [("fig2", lambda o: r.fig2_scenario(r.RowSync(), r.Mode.FINE, o))]
+    for name in ("mlp:1-64", "mlp:1024", "attn:toy", "conv128:1"):
+        gate_scen.append((name, lambda o, n=name: dataclasses.replace(
+            r.build_preset(n, r.PRESETS[n].policies[0]), options=o)))
+    for seed in range(20):
+        gate_scen.append((f"random:{seed}", lambda o, sd=seed: dataclasses.replace(
+            r.random_scenario(sd), options=o)))
+    for name, mk in gate_scen:
+        for wk in ("on", "off", "auto"):
+            sc = mk(r.SimOptions(wait_kernel=wk))
+            eng["gates"].append({
+                "name": name, "wait_kernel": wk, "mode": sc.mode.value,
+                "num_sms": sc.gpu.num_sms,
+                "stages": [stage_dict(st) | {"occupancy": st.occupancy} for st in sc.stages],
+                "deps": [dep_dict(d) for d in sc.deps],
+                "gated": {st.id: list(r.gated_producers(sc, st)) for st in sc.stages},
+                "avoid": [r.avoid_wait_kernel(sc.stage_by_id(d.producer),
+                                              sc.stage_by_id(d.consumer), sc.gpu)
+                          for d in sc.deps]})
+    for vals in itertools.product((0.0, 1.5, 4.0), (1.0, 2.0), (0.5, 3.0), (1.0, 2.5)):
+        for reorder in (False, True):
+            eng["kstep"].append({"args": list(vals), "reorder": reorder,
+                                 "value": r.kstep_duration(*vals, reorder=reorder)})
+    D, S = r.Dim3, r.Stage
+    bad = {
+        "duplicate": ((S("a", D(2, 2, 1)), S("a", D(2, 2, 1))), ()),
+        "unknown": ((S("a", D(2, 2, 1)), S("b", D(2, 2, 1))), (r.Dependency("a", "c"),)),
+        "cycle": ((S("a", D(2, 2, 1)), S("b", D(2, 2, 1))), (r.Dependency("b", "a"),)),
+        "operand": ((S("a", D(2, 2, 1)), S("b", D(2, 2, 1))), (r.Dependency("a", "b", "q"),)),
+        "rows": ((S("a", D(2, 2, 1)), S("b", D(3, 2, 1))), (r.Dependency("a", "b"),)),
+        "tile_ksteps": ((S("a", D(2, 2, 1)), S("b", D(2, 2, 1), k_steps=3)),
+                        (r.Dependency("a", "b", policy=r.TileSync()),)),
+        "conv_kk": ((S("a", D(2, 2, 1)), S("b", D(2, 2, 1), k_steps=10)),
+                    (r.Dependency("a", "b", policy=r.Conv2DTileSync(9)),)),
+        "conv_cols": ((S("a", D(2, 2, 1)), S("b", D(2, 2, 1), k_steps=27)),
+                      (r.Dependency("a", "b", policy=r.Conv2DTileSync(9)),)),
+        "strided": ((S("a", D(2, 6, 1)), S("b", D(2, 2, 1))),
+                    (r.Dependency("a", "b", policy=r.StridedSync(4)),)),
+        "ok": ((S("a", D(2, 2, 1)), S("b", D(2, 2, 1), k_steps=2)),
+               (r.Dependency("a", "b", policy=r.TileSync()),)),
+    }
+    for name, (stages, deps) in bad.items():
+        try:
+            r.Scenario(gpu=r.GpuConfig(4), stages=stages, deps=deps)
+            err = None
+        except Exception as e:  # noqa: BLE001 - recorded as the golden outcome
+            err = [type(e).__name__, str(e)]
+        eng["errors"].append({"name": name, "stages": [stage_dict(st) for st in stages],
+                              "deps": [dep_dict(d) for d in deps], "error": err})
+    (OUT / "engine_layer.json").write_text(json.dumps(eng, indent=0))
     print("wrote", sorted(p.name for p in OUT.glob("*.json")))
 
 
