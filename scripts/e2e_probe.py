@@ -16,11 +16,14 @@ w1 = (torch.randn(H // 2, H, device="cuda") / H ** 0.5).half()
 w2 = (torch.randn(H, H // 2, device="cuda") / (H // 2) ** 0.5).half()
 xh = x.cpu().pin_memory()
 yh = torch.empty(b, H, dtype=torch.half).pin_memory()
-for name, kw in (("512/512 band4", dict(prod_tile_n=512, cons_tile_n=512, cons_order=ts.BandedColumnMajor(4))),
-                 ("512/512 row", dict(prod_tile_n=512, cons_tile_n=512)),
-                 ("256/512 row", dict(prod_tile_n=0, cons_tile_n=512)),
-                 ("256/256 row", dict())):
-    ch = ts.MlpChain(x.clone(), w1, w2, tile_n=256, cta_group=2, **kw)
+for name, kw in (("512/512 row", dict(prod_tile_n=512, cons_tile_n=512)),
+                 ("512/512 row z4/2", dict(prod_tile_n=512, cons_tile_n=512, prod_splits=4, cons_splits=2)),
+                 ("512/512 row z2/2", dict(prod_tile_n=512, cons_tile_n=512, prod_splits=2, cons_splits=2)),
+                 ("256/256 row z4/2", dict(prod_splits=4, cons_splits=2)),
+                 ("cg1 256/256 row z2/1", dict(cta_group=1, prod_splits=2)),
+                 ("cg1 256/256 row", dict(cta_group=1))):
+    kw = dict(dict(tile_n=256, cta_group=2), **kw)
+    ch = ts.MlpChain(x.clone(), w1, w2, **kw)
     plain = time_fn(lambda: (ch.x.copy_(xh, non_blocking=True), ch(), yh.copy_(ch.y, non_blocking=True)))
     over = time_fn(lambda: ch.run_host(xh, yh))
     kern = time_fn(ch)
