@@ -1133,21 +1133,25 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         const size_t plane = static_cast<size_t>(128) * acc_cols;
         float* mine = st.ws + (static_cast<size_t>(tile_id * st.splits + t.tz) * CG + rank) * plane;
         const int span = acc_cols / G;
+        // only rows < m carry data (small batch: a 128-row tile may hold a single row)
+        const int row0 = t.tx * C::kTileM + static_cast<int>(rank) * 128;
+        const int valid = st.m - row0 < 128 ? (st.m - row0 > 0 ? st.m - row0 : 0) : 128;
 #pragma unroll 1
         for (int j = 0; j <= wide; ++j) {
           const int lo = max(eg * span, j * hn), hi = min((eg + 1) * span, (j + 1) * hn);
 #pragma unroll 1
-          for (int x = lo; x < hi; x += 32) {
+          for (int x = lo; x < hi && ew * 32 < valid; x += 32) {  // warp-uniform skip
             uint32_t r[32];
             ptx::tmem_ld_32x32b_x32(tcol(x), r);
             ptx::tmem_ld_wait();
             if constexpr (C::kChunked) {
               // plane rows of this warp are 32 consecutive 128-B rows of chunk x / 32
               float* wbase = mine + (static_cast<size_t>(x / 32) * 128 + ew * 32) * 32;
-              stage_rows(r, [&](int rr, int g) {
-                return reinterpret_cast<uint4*>(wbase + rr * 32 + g * 4);
+              stage_rows(r, [&](int rr, int g) -> uint4* {
+                return ew * 32 + rr < valid ? reinterpret_cast<uint4*>(wbase + rr * 32 + g * 4)
+                                            : nullptr;
               });
-            } else {
+            } else if (rl_row < valid) {
               float* dst = mine + (static_cast<size_t>(x / 32) * 128 + rl_row) * 32;
 #pragma unroll
               for (int q = 0; q < 4; ++q) ptx::st_global_v8(dst + 8 * q, r + 8 * q);
@@ -1174,8 +1178,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
                               static_cast<size_t>(rank) * plane;
           const bool gl = st.epilogue == TS_EPI_GELU;
           const bool rl = st.epilogue == TS_EPI_RELU;
-          const int steps = (acc_cols / 32) * 32;  // chunks x (128 rows / 4)
-          const int row0 = t.tx * C::kTileM + static_cast<int>(rank) * 128;
+          const int nr4 = (valid + 3) / 4;          // 4-row groups holding data
+          const int steps = (acc_cols / 32) * nr4;  // chunks x row groups
           // kSB steps per iteration with every slice's load of every step in flight (the
           // loop is L2-latency bound otherwise: ~1.5 us per round trip under load)
           constexpr int kSB = C::kChunked ? 2 : 4;
@@ -1190,7 +1194,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
 #pragma unroll
               for (int j = 0; j < kSB; ++j) {
                 const int sidx = s0 + j * kEpiWarps;
-                const size_t off = (static_cast<size_t>(sidx >> 5) * 128 + (sidx & 31) * 4) * 32 + lane * 4;
+                const size_t off =
+                    (static_cast<size_t>(sidx / nr4) * 128 + (sidx % nr4) * 4) * 32 + lane * 4;
 #pragma unroll
                 for (int zz = 0; zz < 4; ++zz)
                   v[j][zz] = (sidx < steps && z0 + zz < st.splits)
@@ -1212,7 +1217,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             for (int j = 0; j < kSB; ++j) {
               const int sidx = s0 + j * kEpiWarps;
               if (sidx >= steps) break;
-              const int chunk = sidx >> 5, r0 = (sidx & 31) * 4;
+              const int chunk = sidx / nr4, r0 = (sidx % nr4) * 4;
               float o[4] = {a[j].x, a[j].y, a[j].z, a[j].w};
 #pragma unroll
               for (int q = 0; q < 4; ++q) o[q] = gl ? gelu(o[q]) : (rl ? relu(o[q]) : o[q]);
