@@ -52,11 +52,11 @@ def candidates(m: int, mode: str):
         # normal layout with split-K: weights on the UMMA N side (256 rows per MMA, 2.6x
         # the weight bytes per MMA of the swapped layout); the activation rows pad a
         # 128-row tile and split-K slices fill the SMs
-        if m <= 128:
-            for z1, z2 in ((6, 3), (6, 6), (3, 3), (4, 2)):
-                for pol in pols:
-                    out.append(dict(policy=pol, mode=mode, tile_n=256, cta_group=1,
-                                    prod_splits=z1, cons_splits=z2))
+        for tn_n, zs in ((256, ((6, 3), (6, 6), (3, 3), (4, 2))) if m <= 128 else (256, ()),
+                         (128, ((3, 3), (3, 1), (6, 3), (2, 2)))):
+            for (z1, z2), pol in itertools.product(zs, pols):
+                out.append(dict(policy=pol, mode=mode, tile_n=tn_n, cta_group=1,
+                                prod_splits=z1, cons_splits=z2))
     for cg, tn in ((2, 256), (1, 256), (2, 128), (1, 128)):
         gx = -(-m // (128 * cg))
         orders = [RowMajor()] + ([BandedColumnMajor(min(gx, 4))] if gx > 1 else [])
