@@ -31,7 +31,7 @@ def main():
             res.append((us, f"B={b} swap{tn} z{z1}/{z2} {mode} {type(pol).__name__}: {us:.1f} us "
                             f"({302e6 / us / 1e6:.2f} TB/s) wd={ch.cs.watchdog_fired()}"))
         for (cg, tn), (z1, z2), (mode, pol) in itertools.product(
-                ((1, 256), (1, 128)), ((6, 3), (3, 3), (3, 1), (2, 2), (6, 6)),
+                ((1, 256), (1, 128), (2, 256)), ((6, 3), (3, 3), (3, 1), (6, 6), (12, 6)),
                 (("fused", ts.RowSync()), ("fused", ts.TileSync()), ("stream", ts.RowSync()))):
             ch = ts.MlpChain(x, w1, w2, policy=pol, mode=mode, tile_n=tn, cta_group=cg,
                              prod_splits=z1, cons_splits=z2)

@@ -464,3 +464,16 @@ def test_run_host_overlapped_copies(mode, pt, swap):
         torch.cuda.synchronize()
         assert not ch.cs.watchdog_fired()
         check_close(yh, y_ref, torch.float16)
+
+
+def test_watchdog_reports_an_unsatisfiable_wait():
+    """The device analogue of detect_deadlock (engine.py:614-637): a semaphore that can
+    never reach its expected count (pre-decremented here) makes the waiting consumer
+    abort after the watchdog period and raise the flag instead of hanging the GPU."""
+    x, w1, w2 = make(128, 256, 256, 256, seed=23)
+    ch = ts.MlpChain(x.cuda(), w1.cuda(), w2.cuda(), policy=ts.RowSync(), tile_n=128,
+                     cta_group=1)
+    ch.cs.deps[0].sem.fill_(-1000)  # posts can only bring it to -1000 + expected
+    ch()
+    torch.cuda.synchronize()
+    assert ch.cs.watchdog_fired()
