@@ -196,9 +196,10 @@ typedef struct {
   int trace_cap;
 } ts_chain_desc;
 
-#define TS_SCRATCH_INTS 8
+#define TS_SCRATCH_INTS 16
 /* scratch layout: [0] work counter, [1] CTA exit counter, [2] trace count,
- *                 [3] watchdog flag (1 = a wait timed out), [4..7] reserved */
+ *                 [3] watchdog flag (1 = a wait timed out), [4] dot claim counter,
+ *                 [8 + d] producer posts of dependency d (done watermark), rest reserved */
 
 /* Device trace record (one event of the reference's JSONL schema, engine.py:220-248). */
 typedef struct {

@@ -28,7 +28,7 @@ TS_FLAG_KEEP_SEMS, TS_FLAG_NO_REORDER, TS_FLAG_NO_WATCHDOG = 1, 2, 4
 
 TS_MAX_STAGES = 4
 TS_MAX_DEPS = 4
-TS_SCRATCH_INTS = 8
+TS_SCRATCH_INTS = 16
 
 # Every symbol include/tilesync.h declares (checked by tests/test_abi.py).
 EXPORTS = (

@@ -476,6 +476,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     dp.kb_per_kstep = kb_per_kstep;
     dp.sem_n = ts::sem_count(dd.policy, dd.param, pg);
     dp.consumer = dd.consumer;
+    dp.posts = pg.x * pg.y * pg.z;
     cs.in_dep = i;
     ts::StageParams& pw = p->st[dd.producer];
     pw.out_deps[pw.n_out_deps++] = i;

@@ -111,6 +111,7 @@ struct DepParams {
   int kb_per_kstep;     // consumer K-blocks per reference k-step
   int sem_n;
   int consumer;         // consumer stage index
+  int posts;            // producer posts in one launch (grid x*y*z): the done watermark
 };
 
 struct ChainParams {
@@ -301,6 +302,33 @@ __device__ __forceinline__ void sem_wait5(const ChainParams& p, const int* s0, i
 
 __device__ __forceinline__ void sem_wait(const ChainParams& p, const int* sem, int expected) {
   sem_wait5(p, sem, expected);
+}
+
+// Producer-done watermark (extension, not a reference semantic): every producer post of
+// dependency d also adds 1 to scratch[kDoneBase + d]. Once a consumer observes it at the
+// dependency's total post count, every producer tile's stores are visible to it (the
+// counter's release RMWs form one release sequence) and none of its later waits in this
+// launch can block, so the producer lane stops probing semaphores for d. The counter is
+// loaded together with the semaphores, so an unsatisfied watermark costs no extra round
+// trip. Returns true when the watermark was reached.
+constexpr int kDoneBase = 8;
+
+__device__ __forceinline__ bool sem_wait_dep(const ChainParams& p, int d, const int* s0, int e0,
+                                             const int* s1, int e1, const int* s2, int e2,
+                                             const int* s3, int e3, const int* s4, int e4) {
+  const int vd = ptx::ld_acquire_gpu(p.scratch + kDoneBase + d);
+  const int v0 = ptx::ld_acquire_gpu(s0);
+  const int v1 = s1 ? ptx::ld_acquire_gpu(s1) : 0;
+  const int v2 = s2 ? ptx::ld_acquire_gpu(s2) : 0;
+  const int v3 = s3 ? ptx::ld_acquire_gpu(s3) : 0;
+  const int v4 = s4 ? ptx::ld_acquire_gpu(s4) : 0;
+  if (vd >= p.dep[d].posts) return true;
+  if (v0 < e0) sem_spin(p, s0, e0);
+  if (s1 && v1 < e1) sem_spin(p, s1, e1);
+  if (s2 && v2 < e2) sem_spin(p, s2, e2);
+  if (s3 && v3 < e3) sem_spin(p, s3, e3);
+  if (s4 && v4 < e4) sem_spin(p, s4, e4);
+  return false;
 }
 
 template <typename T>
@@ -510,6 +538,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       uint32_t kq = 0;    // K-blocks issued (full barrier index)
       uint32_t cid = 0;   // commit group of the K-block being issued
       const int group = commit_group(p.flags);
+      uint32_t done_mask = 0;  // dependencies whose producer-done watermark was observed
       // Claim ring entry e for commit group `cid` once the MMAs of the group that last
       // read it are done.
       auto claim = [&](int e) {
@@ -592,7 +621,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           const int* h2 = halo_sem(1, e2);
           const int* h3 = halo_sem(-2, e3);
           const int* h4 = halo_sem(2, e4);
-          sem_wait5(p, dp.sem + w.sem, w.expected, h1, e1, h2, e2, h3, e3, h4, e4);
+          if ((p.flags >> 23) & 1)  // diagnostic flag bit 23: no watermark
+            sem_wait5(p, dp.sem + w.sem, w.expected, h1, e1, h2, e2, h3, e3, h4, e4);
+          else if (!((done_mask >> d) & 1) &&
+                   sem_wait_dep(p, d, dp.sem + w.sem, w.expected, h1, e1, h2, e2, h3, e3, h4, e4))
+            done_mask |= 1u << d;
           if (leader)
             trace_event(p, ptx::global_timer(), 2, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
                         t.ty, t.tz);
@@ -962,6 +995,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           const DepParams& dp = p.dep[d];
           const int idx = post_target(dp.policy, dp.param, tx, ty, Grid3{dp.pgx, dp.pgy, dp.pgz});
           const int old = ptx::atom_add_release_gpu(dp.sem + idx, 1);
+          ptx::atom_add_release_gpu(p.scratch + kDoneBase + d, 1);
           trace_event(p, tnow, 3, ds, tb, -1, d, idx, old + 1, tx, ty);
         }
         trace_event(p, tnow, 4, ds, tb, -1, -1, -1, -1, tx, ty);
@@ -1313,6 +1347,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
               const int idx = post_target(dp.policy, dp.param, t.tx, t.ty,
                                           Grid3{dp.pgx, dp.pgy, dp.pgz});
               const int old = ptx::atom_add_release_gpu(dp.sem + idx, 1);
+              ptx::atom_add_release_gpu(p.scratch + kDoneBase + d, 1);
               trace_event(p, tnow, 3, t.s, t.tb, -1, d, idx, old + 1, t.tx, t.ty, t.tz);
               if (d == st.dot_dep) {
                 // Which dot tiles of this row did this post complete? (the wait of tile
@@ -1390,6 +1425,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       p.scratch[1] = 0;
       p.scratch[4] = 0;  // last-arriver dot claim counter
     }
+    if (threadIdx.x < TS_MAX_DEPS) p.scratch[kDoneBase + threadIdx.x] = 0;  // watermarks
     __threadfence();
   }
 }

@@ -467,12 +467,30 @@ def test_run_host_overlapped_copies(mode, pt, swap):
 
 
 def test_watchdog_reports_an_unsatisfiable_wait():
-    """The device analogue of detect_deadlock (engine.py:614-637): a semaphore that can
-    never reach its expected count (pre-decremented here) makes the waiting consumer
-    abort after the watchdog period and raise the flag instead of hanging the GPU."""
+    """The device analogue of detect_deadlock (engine.py:614-637): a wait that can never
+    be satisfied — GeMM1's row gate (the run_host input semaphore) expecting a copy that
+    is never signalled — makes the waiting tiles abort after the watchdog period and
+    raise the flag instead of hanging the GPU."""
     x, w1, w2 = make(128, 256, 256, 256, seed=23)
     ch = ts.MlpChain(x.cuda(), w1.cuda(), w2.cuda(), policy=ts.RowSync(), tile_n=128,
                      cta_group=1)
+    ch.prod.in_sem = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ch.cs._desc = None
+    ch.cs.set_in_expected(ch.prod, 1)  # never signalled
+    ch()
+    torch.cuda.synchronize()
+    assert ch.cs.watchdog_fired()
+
+
+def test_watchdog_on_a_corrupted_semaphore():
+    """Same, for an inter-stage semaphore that can never reach its count (pre-decremented);
+    the producer-done watermark is disabled (diagnostic flag bit 23) so the consumer can
+    only observe the semaphore itself."""
+    x, w1, w2 = make(128, 256, 256, 256, seed=23)
+    ch = ts.MlpChain(x.cuda(), w1.cuda(), w2.cuda(), policy=ts.RowSync(), tile_n=128,
+                     cta_group=1)
+    ch.cs.extra_flags |= 1 << 23
+    ch.cs._desc = None
     ch.cs.deps[0].sem.fill_(-1000)  # posts can only bring it to -1000 + expected
     ch()
     torch.cuda.synchronize()
