@@ -401,6 +401,41 @@ __device__ __forceinline__ void dot_batch_warp(const StageParams& st, int row0, 
   }
 }
 
+// Split-K reduction of a normal tile, Z slices known at compile time: kS steps (4 rows x
+// 32 columns of one 32-column chunk; lane l: row r0 + l / 8, columns (l % 8) * 4 .. + 4)
+// with all kS x Z float4 loads in flight before any is summed — the loop is bound by L2
+// latency under the MMA streams of the other SMs, so bytes in flight set its speed.
+// emit(sidx, sum) stores step sidx.
+template <int Z, int kS, typename Emit>
+__device__ __forceinline__ void reduce_split_steps(const float* base, size_t zstride, int s0,
+                                                   int sstride, int steps, int nr4, int lane,
+                                                   Emit&& emit) {
+  float4 v[kS][Z];
+#pragma unroll
+  for (int j = 0; j < kS; ++j) {
+    const int sidx = s0 + j * sstride;
+    const size_t off = (static_cast<size_t>(sidx / nr4) * 128 + (sidx % nr4) * 4) * 32 + lane * 4;
+#pragma unroll
+    for (int z = 0; z < Z; ++z)
+      v[j][z] = sidx < steps ? __ldcg(reinterpret_cast<const float4*>(base + z * zstride + off))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int j = 0; j < kS; ++j) {
+    const int sidx = s0 + j * sstride;
+    if (sidx >= steps) break;
+    float4 a = v[j][0];
+#pragma unroll
+    for (int z = 1; z < Z; ++z) {
+      a.x += v[j][z].x;
+      a.y += v[j][z].y;
+      a.z += v[j][z].z;
+      a.w += v[j][z].w;
+    }
+    emit(sidx, a);
+  }
+}
+
 // diagnostic flag bit 12 (no semaphore waits) also skips the external row gates
 __device__ __forceinline__ bool skip_in_gate(const ChainParams& p) { return (p.flags >> 12) & 1; }
 
@@ -1214,8 +1249,37 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           const bool rl = st.epilogue == TS_EPI_RELU;
           const int nr4 = (valid + 3) / 4;          // 4-row groups holding data
           const int steps = (acc_cols / 32) * nr4;  // chunks x row groups
-          // kSB steps per iteration with every slice's load of every step in flight (the
-          // loop is L2-latency bound otherwise: ~1.5 us per round trip under load)
+          auto emit = [&](int sidx, float4 s) {
+            const int chunk = sidx / nr4, r0 = (sidx % nr4) * 4;
+            float o[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) o[q] = gl ? gelu(o[q]) : (rl ? relu(o[q]) : o[q]);
+            const int grow = row0 + r0 + (lane >> 3);
+            if (grow < st.m) {
+              T* dst = reinterpret_cast<T*>(st.c) + static_cast<size_t>(grow) * st.ldc +
+                       t.ty * acc_cols + chunk * 32 + (lane & 7) * 4;
+              *reinterpret_cast<uint2*>(dst) = make_uint2(pack2<T>(o[0], o[1]), pack2<T>(o[2], o[3]));
+            }
+          };
+          const size_t zs = static_cast<size_t>(CG) * plane;
+          const int ss = kEpiWarps;
+          // ~16 float4 loads in flight per lane for the common slice counts (diagnostic
+          // flag bit 20 forces the generic loop)
+          const int zsel = (p.flags >> 20) & 1 ? 0 : st.splits;
+          if (zsel == 2) {
+#pragma unroll 1
+            for (int s0 = warp - 4; s0 < steps; s0 += ss * 8)
+              reduce_split_steps<2, 8>(base, zs, s0, ss, steps, nr4, lane, emit);
+          } else if (zsel == 3) {
+#pragma unroll 1
+            for (int s0 = warp - 4; s0 < steps; s0 += ss * 5)
+              reduce_split_steps<3, 5>(base, zs, s0, ss, steps, nr4, lane, emit);
+          } else if (zsel == 4) {
+#pragma unroll 1
+            for (int s0 = warp - 4; s0 < steps; s0 += ss * 4)
+              reduce_split_steps<4, 4>(base, zs, s0, ss, steps, nr4, lane, emit);
+          } else {
+          // generic slice count: kSB steps per iteration, 4 slices' loads at a time
           constexpr int kSB = C::kChunked ? 2 : 4;
 #pragma unroll 1
           for (int s0 = warp - 4; s0 < steps; s0 += kEpiWarps * kSB) {
@@ -1251,17 +1315,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             for (int j = 0; j < kSB; ++j) {
               const int sidx = s0 + j * kEpiWarps;
               if (sidx >= steps) break;
-              const int chunk = sidx / nr4, r0 = (sidx % nr4) * 4;
-              float o[4] = {a[j].x, a[j].y, a[j].z, a[j].w};
-#pragma unroll
-              for (int q = 0; q < 4; ++q) o[q] = gl ? gelu(o[q]) : (rl ? relu(o[q]) : o[q]);
-              const int grow = row0 + r0 + (lane >> 3);
-              if (grow < st.m) {
-                T* dst = reinterpret_cast<T*>(st.c) + static_cast<size_t>(grow) * st.ldc +
-                         t.ty * acc_cols + chunk * 32 + (lane & 7) * 4;
-                *reinterpret_cast<uint2*>(dst) = make_uint2(pack2<T>(o[0], o[1]), pack2<T>(o[2], o[3]));
-              }
+              emit(sidx, a[j]);
             }
+          }
           }
         }
       } else if (st.epilogue == TS_EPI_SWIGLU) {

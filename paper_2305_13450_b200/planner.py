@@ -66,6 +66,12 @@ def candidates(m: int, mode: str):
         for pol, co, (pw, cw) in itertools.product(pols, orders, widths):
             out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=cg, cons_order=co,
                             prod_tile_n=pw, cons_tile_n=cw))
+        if (cg, tn) == (2, 256) and m >= 512:
+            # Large batch: GeMM1 has fewer double-width tiles than CTA pairs (B=1024: 48
+            # for 74), so its split-K slices fill the idle pairs and finish rows sooner
+            for pol, co, z1 in itertools.product(pols, orders, (2, 3)):
+                out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=cg, cons_order=co,
+                                prod_tile_n=512, cons_tile_n=512, prod_splits=z1))
     return out
 
 

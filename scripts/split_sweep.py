@@ -23,8 +23,8 @@ def main():
         print(f"B={b} cublas {us:.1f} us", flush=True)
         res = []
         for (pt, ct), (z1, z2), (mode, pol) in itertools.product(
-                ((512, 512), (256, 512), (384, 384), (384, 512), (512, 384), (256, 384)),
-                ((1, 1), (2, 1)),
+                ((512, 512), (256, 512)),
+                ((1, 1), (2, 1), (3, 1), (3, 2), (2, 2), (4, 2), (1, 2), (3, 3)),
                 (("fused", ts.RowSync()), ("fused", ts.TileSync()), ("stream", ts.RowSync()))):
             ch = ts.MlpChain(x, w1, w2, policy=pol, mode=mode, tile_n=256, cta_group=2,
                              prod_tile_n=pt, cons_tile_n=ct, prod_splits=z1, cons_splits=z2,
