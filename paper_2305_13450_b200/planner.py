@@ -66,6 +66,12 @@ def candidates(m: int, mode: str):
         for pol, co, (pw, cw) in itertools.product(pols, orders, widths):
             out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=cg, cons_order=co,
                             prod_tile_n=pw, cons_tile_n=cw))
+        if (cg, tn) == (2, 256) and m <= 512:
+            # Mid batch: a handful of 256 x 512 CTA-pair tiles per stage, split-K slices
+            # (weights on the UMMA N side, 256 rows per MMA) to occupy every pair
+            for (z1, z2), pol in itertools.product(((6, 3), (4, 2), (6, 2), (3, 3), (4, 4)), pols):
+                out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=cg,
+                                prod_tile_n=512, cons_tile_n=512, prod_splits=z1, cons_splits=z2))
         if (cg, tn) == (2, 256) and m >= 512:
             # Large batch: GeMM1 has fewer double-width tiles than CTA pairs (B=1024: 48
             # for 74), so its split-K slices fill the idle pairs and finish rows sooner
