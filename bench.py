@@ -335,7 +335,10 @@ def main():
     traffic = None
     prof = ROOT / "profiles" / "roofline_traffic.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get(f"gpt3_mlp_b{b}")
+        # the ncu capture counts only for the configuration it was taken on
+        for rec in json.loads(prof.read_text()).values():
+            if rec["config"] == planner.describe(best) and rec["batch"] == b:
+                traffic = rec["bytes"]
     cpu_baseline = None
     if world == 1:
         cpu_baseline = cpu_baseline_sample(b)
