@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 3
+#define TS_ABI_VERSION 4
 
 /* ---- status codes ---------------------------------------------------------------- */
 typedef enum {
@@ -164,12 +164,35 @@ typedef enum {
                             [m, n]; XDot = Softmax(Q*V)*K per head and row (column-tile
                             local, dropout p = 0); b unused. Tile = rows x tile_n columns
                             (tile_n / 128 heads).                                         */
-  TS_STAGE_CONV2D = 2    /* 3x3 "same" convolution as implicit GeMM (PAPER.md:190-204,
+  TS_STAGE_CONV2D = 2,   /* 3x3 "same" convolution as implicit GeMM (PAPER.md:190-204,
                             461-463): A gathered by an im2col TMA map, K order = input-
                             channel tile (the producer's column tile) outer, filter tap,
                             64-channel block inner, so Conv2DTileSync(9) waits once per
                             producer column tile (policies.py:161-165)                   */
+  TS_STAGE_ALLREDUCE = 3 /* tensor-parallel all-reduce of the producer's output over peer
+                            memory (extension; the "next" row of SURVEY.md §8f): c = this
+                            rank's producer output [m, n] (ldc), summed in place across
+                            ts_chain_desc.peers. Tile = the producer's tile; this rank owns
+                            tiles t with t % world == rank: it waits for tile t's semaphore
+                            on every rank (system-scope acquire over P2P), sums the N
+                            partial tiles in fp32 and stores the result into every rank's
+                            buffer, then adds 1 to every rank's done counter. The only
+                            dependency into it: producer GeMM -> allreduce, TileSync. */
 } ts_stage_kind;
+
+#define TS_MAX_PEERS 8
+
+/* Peer memory of a tensor-parallel group for TS_STAGE_ALLREDUCE (all device pointers
+ * valid in this process: P2P-mapped / IPC-opened / symmetric memory; index = rank). */
+typedef struct {
+  int world, rank;             /* group size (1..TS_MAX_PEERS) and this rank             */
+  void* bufs[TS_MAX_PEERS];    /* rank q's allreduce buffer (its stage c)                */
+  int* sems[TS_MAX_PEERS];     /* rank q's semaphores of the producer -> allreduce dep   */
+  int* done[TS_MAX_PEERS];     /* rank q's arrival counter (int32, zero on entry; kept
+                                  zero): each owner CTA adds 1 per tile it finalized into
+                                  rank q's buffer; rank q's kernel exits once it counts
+                                  every tile (x cta_group) and resets it                 */
+} ts_peer_desc;
 
 typedef struct {
   int producer, consumer; /* stage indices, producer < consumer                 */
@@ -194,6 +217,7 @@ typedef struct {
   int* scratch;  /* device int32[TS_SCRATCH_INTS], zero on first use; kernels restore it */
   void* trace;   /* optional device ts_trace_rec[trace_cap]; NULL = no tracing */
   int trace_cap;
+  const ts_peer_desc* peers; /* TS_STAGE_ALLREDUCE only (host pointer; copied at launch) */
 } ts_chain_desc;
 
 #define TS_SCRATCH_INTS 16

@@ -23,12 +23,13 @@ TS_ORDER_ROW_MAJOR, TS_ORDER_STRIDED_ROW_MAJOR, TS_ORDER_BANDED_COLUMN_MAJOR = r
 TS_DTYPE_F16, TS_DTYPE_BF16 = range(2)
 TS_EPI_NONE, TS_EPI_GELU, TS_EPI_SWIGLU, TS_EPI_RELU = range(4)
 TS_MODE_STREAM, TS_MODE_FUSED = range(2)
-TS_STAGE_GEMM, TS_STAGE_ATTN_DOT, TS_STAGE_CONV2D = range(3)
+TS_STAGE_GEMM, TS_STAGE_ATTN_DOT, TS_STAGE_CONV2D, TS_STAGE_ALLREDUCE = range(4)
 TS_FLAG_KEEP_SEMS, TS_FLAG_NO_REORDER, TS_FLAG_NO_WATCHDOG = 1, 2, 4
 
 TS_MAX_STAGES = 4
 TS_MAX_DEPS = 4
 TS_SCRATCH_INTS = 16
+TS_MAX_PEERS = 8
 
 # Every symbol include/tilesync.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -62,6 +63,14 @@ class DepDesc(ctypes.Structure):
     ]
 
 
+class PeerDesc(ctypes.Structure):
+    _fields_ = [
+        ("world", ctypes.c_int), ("rank", ctypes.c_int),
+        ("bufs", ctypes.c_void_p * TS_MAX_PEERS), ("sems", ctypes.c_void_p * TS_MAX_PEERS),
+        ("done", ctypes.c_void_p * TS_MAX_PEERS),
+    ]
+
+
 class ChainDesc(ctypes.Structure):
     _fields_ = [
         ("n_stages", ctypes.c_int), ("stages", StageDesc * TS_MAX_STAGES),
@@ -70,6 +79,7 @@ class ChainDesc(ctypes.Structure):
         ("swap_ab", ctypes.c_int), ("flags", ctypes.c_int),
         ("num_ctas", ctypes.c_int), ("scratch", ctypes.c_void_p),
         ("trace", ctypes.c_void_p), ("trace_cap", ctypes.c_int),
+        ("peers", ctypes.POINTER(PeerDesc)),
     ]
 
 
@@ -120,7 +130,7 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.ts_abi_version() != 3:
+    if lib.ts_abi_version() != 4:
         raise RuntimeError("libtilesync_b200.so ABI version mismatch")
     _lib = lib
     return lib

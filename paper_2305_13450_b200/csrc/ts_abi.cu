@@ -297,6 +297,54 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       sp.last_arriver = 0;
       continue;
     }
+    if (st.kind == TS_STAGE_ALLREDUCE) {
+      // tensor-parallel all-reduce of the producer's output tiles over peer memory
+      const ts_peer_desc* pr = d->peers;
+      if (pr == nullptr) return fail(TS_ERR_VALUE, "stage %d: the allreduce stage needs peers", s);
+      if (pr->world < 1 || pr->world > TS_MAX_PEERS || pr->rank < 0 || pr->rank >= pr->world)
+        return fail(TS_ERR_VALUE, "stage %d: peers world %d / rank %d invalid", s, pr->world, pr->rank);
+      for (int q = 0; q < pr->world; ++q)
+        if (!pr->bufs[q] || !pr->sems[q] || !pr->done[q] ||
+            (reinterpret_cast<uintptr_t>(pr->bufs[q]) & 15))
+          return fail(TS_ERR_VALUE, "stage %d: peer %d has a null or misaligned pointer", s, q);
+      if (pr->bufs[pr->rank] != st.c)
+        return fail(TS_ERR_VALUE, "stage %d: peers.bufs[rank] must be this stage's c", s);
+      if (swap) return fail(TS_ERR_CONFIG, "stage %d: the allreduce stage needs normal tiles", s);
+      int prod = -1;
+      for (int i = 0; i < d->n_deps; ++i)
+        if (d->deps[i].consumer == s) prod = d->deps[i].producer;
+      if (prod < 0 || prod >= s || d->stages[prod].kind != TS_STAGE_GEMM)
+        return fail(TS_ERR_CONFIG, "stage %d: the allreduce stage needs one earlier GeMM producer", s);
+      const ts_stage_desc& pd = d->stages[prod];
+      if (pd.c != st.c || pd.ldc != st.ldc || pd.m != st.m || pd.epilogue == TS_EPI_SWIGLU ||
+          pd.n != st.n)
+        return fail(TS_ERR_CONFIG, "stage %d: the allreduce stage sums its producer's output in place", s);
+      if (st.ldc % 8) return fail(TS_ERR_VALUE, "stage %d: ldc must be a multiple of 8", s);
+      const ts::StageParams& pp = p->st[prod];
+      sp.kind = ts::kStageAllReduce;
+      sp.c = st.c;
+      sp.m = st.m;
+      sp.n = st.n;
+      sp.ldc = st.ldc;
+      sp.grid_x = pp.grid_x;
+      sp.grid_y = pp.grid_y;
+      sp.ar_cols = out_tile_cols(pd, bn, cg, swap);
+      sp.splits = 1;
+      sp.order = TS_ORDER_ROW_MAJOR;
+      sp.order_stride = 1;
+      sp.epilogue = TS_EPI_NONE;
+      const int tiles = pp.grid_x * pp.grid_y;
+      sp.item_begin = items;
+      items += (tiles - pr->rank + pr->world - 1) / pr->world;  // tiles t % world == rank
+      sp.item_end = items;
+      sp.in_dep = -1;
+      sp.n_out_deps = 0;
+      sp.dot_dep = -1;
+      sp.last_arriver = 0;
+      p->peers = *pr;
+      p->ar_done = tiles * cg;
+      continue;
+    }
     if (st.kind != TS_STAGE_GEMM && st.kind != TS_STAGE_CONV2D)
       return fail(TS_ERR_TYPE, "stage %d: unknown stage kind %d", s, st.kind);
     const bool conv = st.kind == TS_STAGE_CONV2D;
@@ -427,6 +475,31 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
                   cs.grid_x, ps.grid_x);
     if (cs.in_dep >= 0)
       return fail(TS_ERR_CONFIG, "dependency %d: stage %d already has an operand-A dependency", i, dd.consumer);
+    if (cs.kind == ts::kStageAllReduce) {
+      if (dd.policy != ts::kTile)
+        return fail(TS_ERR_CONFIG, "dependency %d: the allreduce stage waits tile by tile (TileSync)", i);
+      if (ps.kind != ts::kStageGemm)
+        return fail(TS_ERR_CONFIG, "dependency %d: the allreduce producer must be a GeMM", i);
+      if (d->mode == TS_MODE_FUSED && dd.sem == nullptr)
+        return fail(TS_ERR_VALUE, "dependency %d: null semaphore array", i);
+      if (d->peers->sems[d->peers->rank] != dd.sem)
+        return fail(TS_ERR_VALUE, "dependency %d: peers.sems[rank] must be this dependency's semaphores", i);
+      ts::DepParams& dp = p->dep[i];
+      dp.sem = dd.sem;
+      dp.policy = dd.policy;
+      dp.param = dd.param;
+      dp.pgx = pg.x;
+      dp.pgy = pg.y;
+      dp.pgz = pg.z;
+      dp.kb_per_kstep = 1;
+      dp.sem_n = ts::sem_count(dd.policy, dd.param, pg);
+      dp.consumer = dd.consumer;
+      dp.posts = pg.x * pg.y * pg.z;
+      cs.in_dep = i;
+      ts::StageParams& pw = p->st[dd.producer];
+      pw.out_deps[pw.n_out_deps++] = i;
+      continue;
+    }
     if (cs.kind == ts::kStageDot && ps.wide)
       return fail(TS_ERR_CONFIG, "dependency %d: a stage feeding the dot stage must use the chain's tile width", i);
     const int cols = ps.kind == ts::kStageDot ? bn : out_tile_cols(d->stages[dd.producer], bn, cg, swap);
@@ -666,13 +739,23 @@ int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
   }
   // Stream mode: the same kernel, one launch per stage, no semaphores — the
   // stream-synchronized baseline (reference Mode.STREAM engine.py:40-42).
+  // An all-reduce stage keeps its dependency: its tiles still wait for the producer
+  // tiles of every rank (peer ranks run their own launches).
   ts::ChainParams q = p;
-  q.n_deps = 0;
   for (int i = 0; i < q.n_stages; ++i) {
-    q.st[i].in_dep = -1;
+    const bool ar = q.st[i].kind == ts::kStageAllReduce;
+    if (!ar) q.st[i].in_dep = -1;
     q.st[i].n_out_deps = 0;
     q.st[i].dot_dep = -1;
+    for (int j = 0; j < p.st[i].n_out_deps; ++j) {
+      const int dd = p.st[i].out_deps[j];
+      if (p.st[p.dep[dd].consumer].kind == ts::kStageAllReduce)
+        q.st[i].out_deps[q.st[i].n_out_deps++] = dd;
+    }
   }
+  bool any_ar = false;
+  for (int i = 0; i < q.n_stages; ++i) any_ar = any_ar || q.st[i].kind == ts::kStageAllReduce;
+  if (!any_ar) q.n_deps = 0;
   for (int i = 0; i < q.n_stages; ++i) {
     q.item_lo = q.st[i].item_begin;
     q.item_hi = q.st[i].item_end;

@@ -54,6 +54,7 @@ constexpr int kPeerRing = 4;
 constexpr uint64_t kWatchdogNs = 4000000000ull;
 constexpr int kStageGemm = 0;  // C = epi(A x B^T) on tcgen05
 constexpr int kStageDot = 1;   // attention's fused softmax-dot over QKV column tiles
+constexpr int kStageAllReduce = 3;  // TP all-reduce of the producer's tiles over peer memory
 constexpr int kStageConv = 2;  // 3x3 "same" Conv2D as implicit GeMM (im2col TMA A operand)
 
 // K-blocks per tcgen05.commit (flags bits 17-18: 1 -> 1, 2 -> 2, 3 -> 4; 0 -> default 2).
@@ -102,6 +103,7 @@ struct StageParams {
   int* in_sem;
   int in_expected;
   int* out_sem;
+  int ar_cols;  // kStageAllReduce: columns of a tile (the producer's tile width)
 };
 
 struct DepParams {
@@ -123,6 +125,8 @@ struct ChainParams {
   ts_trace_rec* trace;
   int trace_cap;
   int flags;
+  ts_peer_desc peers;  // kStageAllReduce: the tensor-parallel group
+  int ar_done;         // tile halves every rank's owners finalize into this rank's buffer
 };
 
 // Tile geometry. Normal layout: UMMA M runs over activation rows (128 per CTA, 256 per
@@ -276,6 +280,23 @@ __device__ __forceinline__ void sem_spin(const ChainParams& p, const int* sem, i
     }
   }
   (void)ptx::ld_acquire_gpu(sem);
+}
+
+// sem_spin at system scope: a semaphore in a peer GPU's memory (all-reduce stage).
+__device__ __forceinline__ void sem_spin_sys(const ChainParams& p, const int* sem, int expected) {
+  const bool watchdog = (p.flags & TS_FLAG_NO_WATCHDOG) == 0;
+  uint64_t t0 = ptx::global_timer();
+  uint32_t ns = 32;
+#pragma unroll 1
+  while (ptx::ld_relaxed_sys(sem) < expected) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+    if (watchdog && ptx::global_timer() - t0 > kWatchdogNs) {
+      atomicExch(&p.scratch[3], 1);
+      break;
+    }
+  }
+  (void)ptx::ld_acquire_sys(sem);
 }
 
 // Block until *s0 >= e0 and, for the optional extra semaphores (nullptr = none), *si >=
@@ -467,6 +488,47 @@ __device__ __forceinline__ Tile decode(const ChainParams& p, int g) {
   return t;
 }
 
+// Sum of one all-reduce tile's rows [r0, r0 + 128) over the group's buffers, stored back
+// into every buffer (thread `tid` of `nthreads`). One 16-byte vector per peer in flight
+// per thread: more (4 peers at once) pushed the 168-register CTA-pair kernel into spills.
+template <typename T>
+__device__ __forceinline__ void allreduce_rows(const ChainParams& p, const StageParams& st, int r0,
+                                            int ty, int tid, int nthreads) {
+  const int world = p.peers.world;
+  const int rows = st.m - r0 < 128 ? st.m - r0 : 128;
+  const int vpr = st.ar_cols / 8;  // 16-byte vectors per tile row
+  const int total = rows > 0 ? rows * vpr : 0;
+  const size_t base = static_cast<size_t>(r0) * st.ldc + static_cast<size_t>(ty) * st.ar_cols;
+  constexpr int kW = 1;  // peers' loads in flight at once
+#pragma unroll 1
+  for (int v = tid; v < total; v += nthreads) {
+    const size_t off = base + static_cast<size_t>(v / vpr) * st.ldc + (v % vpr) * 8;
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int q0 = 0; q0 < world; q0 += kW) {
+      uint4 u[kW];
+#pragma unroll
+      for (int q = 0; q < kW; ++q)
+        if (q0 + q < world)
+          u[q] = ptx::ld_global_cg_v4(reinterpret_cast<const T*>(p.peers.bufs[q0 + q]) + off);
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        if (q0 + q < world) {
+          float f[8];
+          unpack8<T>(u[q], f);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a[i] += f[i];
+        }
+      }
+    }
+    const uint4 o = make_uint4(pack2<T>(a[0], a[1]), pack2<T>(a[2], a[3]), pack2<T>(a[4], a[5]),
+                               pack2<T>(a[6], a[7]));
+#pragma unroll 1
+    for (int q = 0; q < world; ++q)
+      *reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.peers.bufs[q]) + off) = o;
+  }
+}
+
 template <int BN, int CG, typename T, bool SW>
 __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
     chain_kernel(const __grid_constant__ ChainParams p) {
@@ -521,7 +583,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
   }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.n_stages; ++s) {
-      if (p.st[s].kind == kStageDot) continue;  // the pointwise stage has no tensor maps
+      if (p.st[s].kind == kStageDot || p.st[s].kind == kStageAllReduce)
+        continue;  // pointwise stages have no tensor maps
       ptx::tma_prefetch_desc(&p.st[s].tmap_a);
       ptx::tma_prefetch_desc(&p.st[s].tmap_b);
     }
@@ -612,7 +675,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         const StageParams& st = p.st[t.s];
         if (leader)
           trace_event(p, ptx::global_timer(), 0, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
-        if (st.kind == kStageDot) continue;  // pointwise stage: the epilogue warps run it
+        if (st.kind == kStageDot || st.kind == kStageAllReduce)
+          continue;  // pointwise stages: the epilogue warps run them
         // activation (dependent) and weight (independent) tile rows of this CTA
         const int act_row = SW ? t.tx * BN : t.tx * C::kTileM + static_cast<int>(rank) * 128;
         // a double-width tile's second B box (output columns [BN, 2 BN) of the pair
@@ -864,7 +928,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         const int g = ring_take(it, false);
         if (g < 0) break;
         const StageParams& sp = p.st[stage_of(p, g)];
-        if (sp.kind == kStageDot) continue;  // no MMA, no accumulator buffer
+        if (sp.kind == kStageDot || sp.kind == kStageAllReduce)
+          continue;  // no MMA, no accumulator buffer
         const int kblocks = sp.k_blocks / sp.splits;
         const int wide = C::kChunked ? sp.wide : 0;
         // instruction descriptor: N = the stage's columns per MMA (chunked stages)
@@ -1042,6 +1107,31 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       if (g < 0) break;
       const Tile t = decode(p, g);
       const StageParams& st = p.st[t.s];
+      if (st.kind == kStageAllReduce) {
+        // Tensor-parallel all-reduce of one producer tile (extension): this
+        // rank owns tiles lin = tb * world + rank. Wait for the tile's post on every rank
+        // (system-scope acquire over P2P), sum the world partial tiles in fp32, store the
+        // sum into every rank's buffer, then count the tile into every rank's done counter.
+        // Each CTA of a pair handles its 128 rows.
+        const int world = p.peers.world;
+        const int lin = t.tb * world + p.peers.rank;
+        const int tx = lin / st.grid_y, ty = lin % st.grid_y;
+        const DepParams& dp = p.dep[st.in_dep];
+        if (threadIdx.x == 128) {
+          const int idx = post_target(dp.policy, dp.param, tx, ty, Grid3{dp.pgx, dp.pgy, dp.pgz});
+          for (int q = 0; q < world; ++q) sem_spin_sys(p, p.peers.sems[q] + idx, dp.pgz);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        ptx::fence_acq_rel_sys();
+        allreduce_rows<T>(p, st, tx * C::kTileM + static_cast<int>(rank) * 128, ty,
+                          threadIdx.x - 128, kEpiThreads);
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        if (threadIdx.x == 128) {
+          __threadfence_system();
+          for (int q = 0; q < world; ++q) ptx::atom_add_release_sys(p.peers.done[q], 1);
+        }
+        continue;
+      }
       if (st.kind == kStageDot) {
         // Attention's fused dot: XDot = Dropout(Softmax(XQ . XV)) . XK,
         // column-tile local as its StridedSync dependency defines it — tile (r, h) reads
@@ -1402,7 +1492,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
               const DepParams& dp = p.dep[d];
               const int idx = post_target(dp.policy, dp.param, t.tx, t.ty,
                                           Grid3{dp.pgx, dp.pgy, dp.pgz});
-              const int old = ptx::atom_add_release_gpu(dp.sem + idx, 1);
+              // an all-reduce consumer reads this semaphore (and the tile) from peer GPUs
+              const bool sys = p.st[dp.consumer].kind == kStageAllReduce;
+              if (sys) __threadfence_system();
+              const int old = sys ? ptx::atom_add_release_sys(dp.sem + idx, 1)
+                                  : ptx::atom_add_release_gpu(dp.sem + idx, 1);
               ptx::atom_add_release_gpu(p.scratch + kDoneBase + d, 1);
               trace_event(p, tnow, 3, t.s, t.tb, -1, d, idx, old + 1, t.tx, t.ty, t.tz);
               if (d == st.dot_dep) {
@@ -1472,9 +1566,28 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
   __syncthreads();
   if (*last_flag) {
     __threadfence();
+    // All-reduce stage in this launch: every owner (on every rank) has finalized its
+    // tiles into this rank's buffer once the done counter is complete — and has then
+    // finished reading this rank's semaphores, so they may be reset below.
+    bool ar_here = false;
+    for (int s = 0; s < p.n_stages; ++s)
+      if (p.st[s].kind == kStageAllReduce && p.st[s].item_begin >= p.item_lo &&
+          p.st[s].item_end <= p.item_hi)
+        ar_here = true;
+    if (ar_here) {
+      if (threadIdx.x == 0) {
+        sem_spin_sys(p, p.peers.done[p.peers.rank], p.ar_done);
+        *p.peers.done[p.peers.rank] = 0;
+      }
+      __syncthreads();
+    }
     if ((p.flags & TS_FLAG_KEEP_SEMS) == 0) {
-      for (int d = 0; d < p.n_deps; ++d)
+      for (int d = 0; d < p.n_deps; ++d) {
+        // a dependency read from peer GPUs is reset only by the launch that ran its
+        // all-reduce consumer (stream mode launches stages one by one)
+        if (p.st[p.dep[d].consumer].kind == kStageAllReduce && !ar_here) continue;
         for (int i = threadIdx.x; i < p.dep[d].sem_n; i += C::kThreads) p.dep[d].sem[i] = 0;
+      }
     }
     if (threadIdx.x == 0) {
       p.scratch[0] = 0;

@@ -61,7 +61,8 @@ class CuStage:
     splits: int = 1
     ws: torch.Tensor | None = None
     cnt: torch.Tensor | None = None
-    kind: str = "gemm"  # "gemm", "dot" (attention's fused softmax-dot) or "conv"
+    kind: str = "gemm"  # "gemm", "dot" (attention's fused softmax-dot), "conv" or
+    # "allreduce" (tensor-parallel sum of its producer's output over peer memory)
     conv: tuple | None = None  # (N, H, W) of a 3x3 "same" convolution stage
     in_sem: torch.Tensor | None = None   # external row gate on operand A (ts_stream_signal)
     out_sem: torch.Tensor | None = None  # per-row "tiles stored" counters (ts_stream_wait)
@@ -74,7 +75,7 @@ class CuStage:
     @property
     def n(self) -> int:
         """Output columns (accumulator columns for SwiGLU)."""
-        return self.c.shape[1] if self.kind == "dot" else self.b.shape[0]
+        return self.c.shape[1] if self.kind in ("dot", "allreduce") else self.b.shape[0]
 
     @property
     def k(self) -> int:
@@ -100,7 +101,7 @@ class CuStage:
         return Dim3(-(-self.m // self.cs.tile_m), max(1, self.n // self.width), self.splits)
 
     def flops(self) -> int:
-        return 0 if self.kind == "dot" else 2 * self.m * self.n * self.k
+        return 0 if self.kind in ("dot", "allreduce") else 2 * self.m * self.n * self.k
 
 
 @dataclass
@@ -145,6 +146,8 @@ class CuSync:
         if self.cta_group not in (1, 2) or (self.cta_group == 2 and self.tile_n == 64):
             raise ConfigError("cta_group must be 1 or 2 (2 needs tile_n >= 128)")
         self._desc: _lib.ChainDesc | None = None
+        self._peers: _lib.PeerDesc | None = None
+        self._ar_done: torch.Tensor | None = None
         self._scratch: torch.Tensor | None = None
         self._trace: torch.Tensor | None = None
         self._trace_cap = 0
@@ -262,6 +265,55 @@ class CuSync:
         self._desc = None
         return st
 
+    def stage_allreduce(self, producer: CuStage, id: str | None = None) -> CuStage:
+        """Tensor-parallel all-reduce of ``producer``'s output, fused into the chain
+        (extension; SURVEY.md §8f "next"): the producer's output buffer is summed in place
+        across the group given by ``set_peers``. This rank owns the producer tiles t with
+        t % world == rank; an owned tile waits for its post on every rank (system-scope
+        acquire), is summed over the ranks' buffers in fp32 and stored back into all of
+        them — the reduction of a row tile starts as soon as every rank has produced it,
+        instead of after the whole GeMM. Adds the producer -> all-reduce TileSync
+        dependency."""
+        from .policies import TileSync
+        if len(self.stages) >= _lib.TS_MAX_STAGES:
+            raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
+        if producer.kind != "gemm" or producer.epilogue == "swiglu" or self.swap_ab:
+            raise ConfigError("the all-reduce stage sums a normal-layout GeMM stage's output")
+        c = producer.c
+        st = CuStage(self, len(self.stages), id or "allreduce", c, c, c, "none", RowMajor(),
+                     kind="allreduce", tile_n=producer.tile_n)
+        self.stages.append(st)
+        self.dependency(TileSync(), producer, st)
+        self._ar_done = torch.zeros(1, dtype=torch.int32, device=c.device)
+        self._desc = None
+        return st
+
+    @property
+    def allreduce_done(self) -> torch.Tensor:
+        """This rank's all-reduce arrival counter (zero between launches)."""
+        return self._ar_done
+
+    def allreduce_dep(self) -> "CuDep":
+        return next(d for d in self.deps if d.consumer.kind == "allreduce")
+
+    def set_peers(self, rank: int, bufs, sems, dones) -> None:
+        """The tensor-parallel group of the all-reduce stage: for every rank q, its
+        buffer (the all-reduce stage's c), its producer -> all-reduce semaphores and its
+        done counter, as device pointers valid in this process (ints or tensors: P2P /
+        IPC-mapped / symmetric memory; on one GPU, plain tensors simulate the group)."""
+        world = len(bufs)
+        if not (1 <= world <= _lib.TS_MAX_PEERS) or len(sems) != world or len(dones) != world:
+            raise ConfigError(f"peer lists must have 1..{_lib.TS_MAX_PEERS} equal entries")
+        if not 0 <= rank < world:
+            raise ConfigError(f"rank {rank} outside world {world}")
+        ptr = (lambda v: v.data_ptr() if isinstance(v, torch.Tensor) else int(v))
+        pd = _lib.PeerDesc()
+        pd.world, pd.rank = world, rank
+        for q in range(world):
+            pd.bufs[q], pd.sems[q], pd.done[q] = ptr(bufs[q]), ptr(sems[q]), ptr(dones[q])
+        self._peers = pd
+        self._desc = None
+
     def dependency(self, policy: SyncPolicy, producer: CuStage, consumer: CuStage,
                    operand: str = "a") -> CuDep:
         """cs.dependency<Policy>(prod, cons, operand) — allocates the semaphore array."""
@@ -280,6 +332,8 @@ class CuSync:
         in_dep = {d.consumer.index: d for d in self.deps}
         stages = []
         for st in self.stages:
+            if st.kind == "allreduce":
+                continue  # the collective is outside the reference model
             d = in_dep.get(st.index)
             if st.kind == "dot":
                 k_steps = 1  # attention_scenario's dot stage (workloads.py:124-153)
@@ -293,7 +347,7 @@ class CuSync:
             stages.append(Stage(id=st.id, grid=st.grid, occupancy=1, k_steps=k_steps,
                                 order=st.order, operands=operands))
         deps = tuple(Dependency(d.producer.id, d.consumer.id, d.operand, d.policy)
-                     for d in self.deps)
+                     for d in self.deps if d.consumer.kind != "allreduce")
         mode = Mode.FINE if self.mode == "fused" else Mode.STREAM
         return Scenario(gpu=GpuConfig(num_sms), stages=tuple(stages), deps=deps, mode=mode)
 
@@ -312,8 +366,8 @@ class CuSync:
             sd.epilogue = _EPI[st.epilogue]
             sd.order, sd.order_stride = order_code(st.order)
             sd.splits = st.splits
-            sd.kind = {"dot": _lib.TS_STAGE_ATTN_DOT, "conv": _lib.TS_STAGE_CONV2D}.get(
-                st.kind, _lib.TS_STAGE_GEMM)
+            sd.kind = {"dot": _lib.TS_STAGE_ATTN_DOT, "conv": _lib.TS_STAGE_CONV2D,
+                       "allreduce": _lib.TS_STAGE_ALLREDUCE}.get(st.kind, _lib.TS_STAGE_GEMM)
             if st.conv is not None:
                 sd.conv_n, sd.conv_h, sd.conv_w = st.conv
             sd.in_sem = st.in_sem.data_ptr() if st.in_sem is not None else None
@@ -346,6 +400,10 @@ class CuSync:
         d.scratch = self._scratch.data_ptr()
         d.trace = None
         d.trace_cap = 0
+        if any(st.kind == "allreduce" for st in self.stages):
+            if getattr(self, "_peers", None) is None:
+                raise ConfigError("the all-reduce stage needs set_peers(...) before launch")
+            d.peers = ctypes.pointer(self._peers)
         return d
 
     def enable_trace(self, capacity: int | None = None) -> None:

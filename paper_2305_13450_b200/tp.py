@@ -64,3 +64,51 @@ class TPMlp:
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
             dist.all_reduce(y, op=dist.ReduceOp.SUM, group=self.group)
         return y
+
+
+class FusedTPMlp:
+    """One rank of a tensor-parallel MLP with the all-reduce fused into the chain
+    (SURVEY.md §8f): GeMM1 -> GeLU -> GeMM2 -> all-reduce in one persistent launch. The
+    all-reduce stage sums GeMM2's output tiles across the group over peer memory as soon
+    as every rank has posted them (``CuSync.stage_allreduce``), so the reduction of early
+    tiles overlaps the GeMMs of later ones instead of waiting for the whole chain and an
+    NCCL call. Tile ownership is round-robin (tile t belongs to rank t % world).
+
+    Peers are connected with ``connect_group`` (one process addressing every member's
+    memory: a single GPU simulating the group, or one process driving P2P-enabled GPUs);
+    a multi-process group passes IPC-mapped / symmetric-memory pointers to
+    ``cs.set_peers`` (``handles`` lists what each rank must publish).
+    """
+
+    def __init__(self, x: torch.Tensor, w1_shard: torch.Tensor, w2_shard: torch.Tensor,
+                 policy: SyncPolicy = RowSync(), **chain_kw):
+        self.chain = MlpChain(x, w1_shard, w2_shard, policy=policy, **chain_kw)
+        self.ar = self.chain.cs.stage_allreduce(self.chain.cons)
+
+    @property
+    def y(self) -> torch.Tensor:
+        return self.chain.y
+
+    def handles(self) -> tuple[int, int, int]:
+        """(buffer, semaphores, done counter) device pointers this rank publishes."""
+        cs = self.chain.cs
+        return (self.chain.y.data_ptr(), cs.allreduce_dep().sem.data_ptr(),
+                cs.allreduce_done.data_ptr())
+
+    def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        return self.chain(stream)
+
+
+def connect_group(members: list[FusedTPMlp]) -> None:
+    """Give every member of a single-process group the others' buffers, semaphores and
+    done counters (rank = list position)."""
+    hs = [m.handles() for m in members]
+    bufs, sems, dones = ([h[i] for h in hs] for i in range(3))
+    for r, m in enumerate(members):
+        m.chain.cs.set_peers(r, bufs, sems, dones)
+
+
+def owned_tiles(tiles: int, rank: int, world: int) -> list[int]:
+    """Producer tiles whose all-reduce rank `rank` performs (the kernel's ownership rule:
+    item i of the all-reduce stage is tile i * world + rank)."""
+    return list(range(rank, tiles, world))

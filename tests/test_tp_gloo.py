@@ -70,3 +70,13 @@ def test_shard_shapes_and_errors():
         pass
     else:
         raise AssertionError("expected ValueError")
+
+
+def test_allreduce_ownership_rule():
+    """The fused all-reduce stage's ownership (item i of rank r = tile i * world + r):
+    every producer tile is reduced by exactly one rank."""
+    from paper_2305_13450_b200 import tp
+    for tiles in (1, 7, 48, 96):
+        for world in (1, 2, 3, 8):
+            owned = [t for r in range(world) for t in tp.owned_tiles(tiles, r, world)]
+            assert sorted(owned) == list(range(tiles))
