@@ -45,9 +45,10 @@ def test_struct_layout_matches_header(tmp_path):
         #include <stddef.h>
         #include "tilesync.h"
         int main(void) {
-          printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(ts_stage_desc), sizeof(ts_dep_desc),
+          printf("%zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(ts_stage_desc), sizeof(ts_dep_desc),
                  sizeof(ts_chain_desc), sizeof(ts_trace_rec),
-                 offsetof(ts_chain_desc, scratch), offsetof(ts_trace_rec, clk));
+                 offsetof(ts_chain_desc, scratch), offsetof(ts_trace_rec, clk),
+                 sizeof(ts_peer_desc), offsetof(ts_chain_desc, peers));
           return 0;
         }"""))
     exe = tmp_path / "sz"
@@ -56,7 +57,8 @@ def test_struct_layout_matches_header(tmp_path):
                                           check=True).stdout.split()]
     want = [ctypes.sizeof(_lib.StageDesc), ctypes.sizeof(_lib.DepDesc),
             ctypes.sizeof(_lib.ChainDesc), ctypes.sizeof(_lib.TraceRec),
-            _lib.ChainDesc.scratch.offset, _lib.TraceRec.clk.offset]
+            _lib.ChainDesc.scratch.offset, _lib.TraceRec.clk.offset,
+            ctypes.sizeof(_lib.PeerDesc), _lib.ChainDesc.peers.offset]
     assert got == want
 
 
@@ -119,3 +121,52 @@ def test_descriptor_validation_maps_to_reference_errors():
         grid_of(_desc(tile_n=96), 0)
     # TileSync needs one producer column tile per consumer k-step (engine.py:157-160)
     assert grid_of(_desc(policy=_lib.TS_POLICY_TILE), 1) == (2, 4)
+
+
+def _allreduce_desc(world=2, rank=0, policy=_lib.TS_POLICY_TILE):
+    """MLP chain + all-reduce stage over GeMM2's output (nothing is dereferenced)."""
+    d = _desc(cta_group=2)
+    d.n_stages = 3
+    y = 2 << 20
+    d.stages[1].c = y
+    ar = d.stages[2]
+    ar.a = ar.b = ar.c = y
+    ar.m, ar.n, ar.k, ar.lda, ar.ldb, ar.ldc = 256, 1024, 1024, 1024, 1024, 1024
+    ar.dtype = _lib.TS_DTYPE_F16
+    ar.kind = _lib.TS_STAGE_ALLREDUCE
+    d.n_deps = 2
+    dep = d.deps[1]
+    dep.producer, dep.consumer, dep.operand, dep.policy, dep.param = 1, 2, 0, policy, 0
+    dep.sem = 3 << 20
+    pd = _lib.PeerDesc()
+    pd.world, pd.rank = world, rank
+    for q in range(world):
+        pd.bufs[q] = y if q == rank else (4 + q) << 20
+        pd.sems[q] = dep.sem if q == rank else (12 + q) << 20
+        pd.done[q] = (20 + q) << 20
+    d.peers = ctypes.pointer(pd)
+    d._keep = pd
+    return d
+
+
+def test_allreduce_stage_validation():
+    """TS_STAGE_ALLREDUCE (fused TP all-reduce): tiles = the producer's; descriptor errors
+    map onto the reference's exception types."""
+    assert grid_of(_allreduce_desc(), 2) == grid_of(_allreduce_desc(), 1)
+    d = _allreduce_desc()
+    d.peers = None
+    with pytest.raises(ValueError):
+        grid_of(d, 2)
+    with pytest.raises(ConfigError):  # the all-reduce waits tile by tile
+        grid_of(_allreduce_desc(policy=_lib.TS_POLICY_ROW), 2)
+    with pytest.raises(ValueError):  # rank outside the group
+        grid_of(_allreduce_desc(world=2, rank=2), 2)
+    d = _allreduce_desc()
+    d._keep.bufs[0] = 9 << 20  # peers.bufs[rank] must be the stage's own buffer
+    with pytest.raises(ValueError):
+        grid_of(d, 2)
+    d = _allreduce_desc()
+    d.stages[2].c = d.stages[2].a = 7 << 20  # sums its producer's output in place
+    d._keep.bufs[0] = 7 << 20
+    with pytest.raises(ConfigError):
+        grid_of(d, 2)
