@@ -11,13 +11,14 @@ s, cg, z = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 pol = {"row": ts.RowSync(), "tile": ts.TileSync()}[sys.argv[4]]
 flags = int(sys.argv[5], 0) if len(sys.argv) > 5 else 0
 mode = sys.argv[6] if len(sys.argv) > 6 else "fused"
+ow = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 hidden, heads = 12288, 12
 torch.manual_seed(8)
 wqkv = (torch.randn(3 * heads * 128, hidden, device="cuda") / hidden ** 0.5).half()
 w2 = (torch.randn(hidden, heads * 128, device="cuda") / (heads * 128) ** 0.5).half()
 x = torch.randn(s, hidden, device="cuda").half()
 ch = ts.AttentionChain(x, wqkv, w2, second_policy=pol, cta_group=cg, qkv_splits=z,
-                       extra_flags=flags, mode=mode)
+                       extra_flags=flags, mode=mode, out_tile_n=ow)
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 for _ in range(3):
     ch()
