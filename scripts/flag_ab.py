@@ -23,11 +23,14 @@ def chains():
         x = torch.randn(b, H, device="cuda").half()
         for pol in (ts.RowSync(), ts.TileSync()):
             yield f"mlp B={b} {type(pol).__name__}", ts.MlpChain(x, w1, w2, policy=pol, **kw)
-    for n, hw, c, tn, cg in ((32, 56, 64, 64, 1), (32, 28, 128, 128, 1), (32, 14, 256, 256, 2),
-                             (32, 7, 512, 256, 2)):
+    for n, hw, c, tn, cg, z in ((32, 56, 64, 64, 1, 1), (32, 28, 128, 128, 1, 1),
+                                (32, 14, 256, 256, 2, 1), (32, 7, 512, 256, 2, 1),
+                                (1, 7, 512, 64, 1, 4), (8, 7, 512, 128, 1, 4),
+                                (1, 14, 256, 64, 1, 4)):
         x = torch.randn(n, hw, hw, c, device="cuda").half()
         wc = (torch.randn(c, 3, 3, c, device="cuda") / (9 * c) ** 0.5).half()
-        yield f"conv {n}x{hw}x{c}", ts.ConvChain(x, wc, wc.clone(), tile_n=tn, cta_group=cg)
+        yield f"conv {n}x{hw}x{c} z{z}", ts.ConvChain(x, wc, wc.clone(), tile_n=tn, cta_group=cg,
+                                                      prod_splits=z, cons_splits=z)
     x = torch.randn(512, H, device="cuda").half()
     wq = (torch.randn(3 * 12 * 128, H, device="cuda") / H ** 0.5).half()
     wo = (torch.randn(H, 12 * 128, device="cuda") / (12 * 128) ** 0.5).half()
