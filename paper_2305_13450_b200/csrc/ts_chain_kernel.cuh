@@ -430,7 +430,7 @@ __device__ __forceinline__ void dot_batch_warp(const StageParams& st, int row0, 
 template <int Z, int kS, typename Emit>
 __device__ __forceinline__ void reduce_split_steps(const float* base, size_t zstride, int s0,
                                                    int sstride, int steps, int nr4, int lane,
-                                                   Emit&& emit) {
+                                                   uint64_t pol, Emit&& emit) {
   float4 v[kS][Z];
 #pragma unroll
   for (int j = 0; j < kS; ++j) {
@@ -438,7 +438,7 @@ __device__ __forceinline__ void reduce_split_steps(const float* base, size_t zst
     const size_t off = (static_cast<size_t>(sidx / nr4) * 128 + (sidx % nr4) * 4) * 32 + lane * 4;
 #pragma unroll
     for (int z = 0; z < Z; ++z)
-      v[j][z] = sidx < steps ? __ldcg(reinterpret_cast<const float4*>(base + z * zstride + off))
+      v[j][z] = sidx < steps ? ptx::ld_global_cg_f4_hint(base + z * zstride + off, pol)
                              : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 #pragma unroll
@@ -1045,7 +1045,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
     // and come back as 4 rows x 128 B per instruction, written with 16-B stores to
     // dst(row_in_warp, granule) (nullptr = skip).
     uint32_t* stg = reinterpret_cast<uint32_t*>(smem + C::kStageOff + (warp - 4) * 4096);
+    // split-K partial planes: written evict_last, read evict_first, so they stay in L2
+    // between the slices instead of round-tripping through HBM under the weight streams
+    // (diagnostic flag bit 26: no hints)
     auto stage_rows = [&](const uint32_t (&v)[32], auto&& dst) {
+      const uint64_t pol_el =
+          (p.flags >> 26) & 1 ? ptx::policy_evict_normal() : ptx::policy_evict_last();
 #pragma unroll
       for (int g = 0; g < 8; ++g)
         *reinterpret_cast<uint4*>(stg + lane * 32 + ((g ^ (lane & 7)) * 4)) =
@@ -1056,7 +1061,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         const int rr = 4 * i + (lane >> 3), g = lane & 7;
         const uint4 q = *reinterpret_cast<const uint4*>(stg + rr * 32 + ((g ^ (rr & 7)) * 4));
         uint4* d = dst(rr, g);
-        if (d != nullptr) *d = q;
+        if (d != nullptr) ptx::st_global_v4_hint(d, q, pol_el);
       }
       __syncwarp();
     };
@@ -1353,21 +1358,23 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           };
           const size_t zs = static_cast<size_t>(CG) * plane;
           const int ss = kEpiWarps;
+          const uint64_t pol_ef =
+              (p.flags >> 26) & 1 ? ptx::policy_evict_normal() : ptx::policy_evict_first();
           // ~16 float4 loads in flight per lane for the common slice counts (diagnostic
           // flag bit 20 forces the generic loop)
           const int zsel = (p.flags >> 20) & 1 ? 0 : st.splits;
           if (zsel == 2) {
 #pragma unroll 1
             for (int s0 = warp - 4; s0 < steps; s0 += ss * 8)
-              reduce_split_steps<2, 8>(base, zs, s0, ss, steps, nr4, lane, emit);
+              reduce_split_steps<2, 8>(base, zs, s0, ss, steps, nr4, lane, pol_ef, emit);
           } else if (zsel == 3) {
 #pragma unroll 1
             for (int s0 = warp - 4; s0 < steps; s0 += ss * 5)
-              reduce_split_steps<3, 5>(base, zs, s0, ss, steps, nr4, lane, emit);
+              reduce_split_steps<3, 5>(base, zs, s0, ss, steps, nr4, lane, pol_ef, emit);
           } else if (zsel == 4) {
 #pragma unroll 1
             for (int s0 = warp - 4; s0 < steps; s0 += ss * 4)
-              reduce_split_steps<4, 4>(base, zs, s0, ss, steps, nr4, lane, emit);
+              reduce_split_steps<4, 4>(base, zs, s0, ss, steps, nr4, lane, pol_ef, emit);
           } else {
           // generic slice count: kSB steps per iteration, 4 slices' loads at a time
           constexpr int kSB = C::kChunked ? 2 : 4;

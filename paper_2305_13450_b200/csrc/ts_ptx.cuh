@@ -272,6 +272,23 @@ __device__ __forceinline__ uint4 ld_global_cg_v4(const void* p) {
   return v;
 }
 
+// 128-bit global store with an L2 cache-policy hint (createpolicy): split-K partial
+// planes are written evict_last so they are still in L2 when the summing slice reads them.
+__device__ __forceinline__ void st_global_v4_hint(void* p, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+
+// 128-bit L2-only load with a cache-policy hint (evict_first: a partial plane dies here).
+__device__ __forceinline__ float4 ld_global_cg_f4_hint(const float* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
 // 256-bit global store (sm_100: STG.256, one full 32-B sector per lane).
 __device__ __forceinline__ void st_global_v8(void* p, const uint32_t* v) {
   asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
