@@ -24,11 +24,11 @@ from oracle import tilesync_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def make(m, k, n1, n2, seed=0):
+def make(m, k, n1, n2, seed=0, dtype=torch.float16):
     g = torch.Generator().manual_seed(seed)
-    x = torch.randn(m, k, generator=g).half()
-    w1 = (torch.randn(n1, k, generator=g) / k ** 0.5).half()
-    w2 = (torch.randn(n2, n1, generator=g) / n1 ** 0.5).half()
+    x = torch.randn(m, k, generator=g).to(dtype)
+    w1 = (torch.randn(n1, k, generator=g) / k ** 0.5).to(dtype)
+    w2 = (torch.randn(n2, n1, generator=g) / n1 ** 0.5).to(dtype)
     return x, w1, w2
 
 
@@ -67,7 +67,7 @@ def run_group(x, w1, w2, world, mode="fused", **kw):
 def test_fused_allreduce_matches_sum_of_partials(world, mode, kw):
     x, w1, w2 = make(512, 1024, 2048, 1024, seed=world)
     members, parts = run_group(x, w1, w2, world, mode, **kw)
-    expect = sum(p.float() for p in parts).half()
+    expect = sum(p.float() for p in parts).to(parts[0].dtype)
     for m in members:
         assert not m.chain.cs.watchdog_fired()
         assert torch.equal(m.y, expect)
@@ -78,3 +78,15 @@ def test_fused_allreduce_matches_sum_of_partials(world, mode, kw):
     err = np.abs(members[0].y.float().cpu().numpy() - ref)
     assert (err <= 2e-2 * world + 1e-2 * np.abs(ref)).all(), err.max()
 
+
+
+def test_fused_allreduce_bf16_ragged_rows():
+    """bf16, a row count that is not a multiple of the tile (partial last row tile), 3 ranks
+    (a world that does not divide the tile count)."""
+    x, w1, w2 = make(300, 512, 1536, 768, seed=9, dtype=torch.bfloat16)
+    members, parts = run_group(x, w1, w2, 3, "fused", tile_n=256, cta_group=2)
+    expect = sum(p.float() for p in parts).to(torch.bfloat16)
+    for m in members:
+        assert not m.chain.cs.watchdog_fired()
+        assert torch.equal(m.y, expect)
+        assert int(m.chain.cs.allreduce_done.item()) == 0
