@@ -489,43 +489,58 @@ __device__ __forceinline__ Tile decode(const ChainParams& p, int g) {
 }
 
 // Sum of one all-reduce tile's rows [r0, r0 + 128) over the group's buffers, stored back
-// into every buffer (thread `tid` of `nthreads`). One 16-byte vector per peer in flight
-// per thread: more (4 peers at once) pushed the 168-register CTA-pair kernel into spills.
+// into every buffer (thread `tid` of `nthreads`). The peers' 16-byte vectors are staged
+// with cp.async into `stage` (the operand ring, idle by the time an all-reduce item reaches
+// the epilogue: every earlier GeMM item of this CTA has drained it and all later items
+// are all-reduce items), up to 8 vectors x world per thread in flight without registers —
+// the loop is bound by the latency of peer (NVLink) or HBM reads otherwise.
 template <typename T>
 __device__ __forceinline__ void allreduce_rows(const ChainParams& p, const StageParams& st, int r0,
-                                            int ty, int tid, int nthreads) {
+                                               int ty, int tid, int nthreads, uint8_t* stage,
+                                               int stage_bytes) {
   const int world = p.peers.world;
   const int rows = st.m - r0 < 128 ? st.m - r0 : 128;
   const int vpr = st.ar_cols / 8;  // 16-byte vectors per tile row
   const int total = rows > 0 ? rows * vpr : 0;
   const size_t base = static_cast<size_t>(r0) * st.ldc + static_cast<size_t>(ty) * st.ar_cols;
-  constexpr int kW = 1;  // peers' loads in flight at once
+  const int slots = stage_bytes / (16 * nthreads) / world;  // vectors per thread in flight
+  const int nb = slots > 8 ? 8 : (slots < 1 ? 1 : slots);
+  uint4* sv = reinterpret_cast<uint4*>(stage);  // slot (i * world + q) * nthreads + tid
+  auto offset = [&](int v) {
+    return base + static_cast<size_t>(v / vpr) * st.ldc + (v % vpr) * 8;
+  };
 #pragma unroll 1
-  for (int v = tid; v < total; v += nthreads) {
-    const size_t off = base + static_cast<size_t>(v / vpr) * st.ldc + (v % vpr) * 8;
-    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int v0 = 0; v0 < total; v0 += nb * nthreads) {
 #pragma unroll 1
-    for (int q0 = 0; q0 < world; q0 += kW) {
-      uint4 u[kW];
-#pragma unroll
-      for (int q = 0; q < kW; ++q)
-        if (q0 + q < world)
-          u[q] = ptx::ld_global_cg_v4(reinterpret_cast<const T*>(p.peers.bufs[q0 + q]) + off);
-#pragma unroll
-      for (int q = 0; q < kW; ++q) {
-        if (q0 + q < world) {
-          float f[8];
-          unpack8<T>(u[q], f);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) a[i] += f[i];
-        }
-      }
+    for (int i = 0; i < nb; ++i) {
+      const int v = v0 + i * nthreads + tid;
+      if (v >= total) break;
+      const size_t off = offset(v);
+#pragma unroll 1
+      for (int q = 0; q < world; ++q)
+        ptx::cp_async16(ptx::smem_u32(&sv[(i * world + q) * nthreads + tid]),
+                        reinterpret_cast<const T*>(p.peers.bufs[q]) + off);
     }
-    const uint4 o = make_uint4(pack2<T>(a[0], a[1]), pack2<T>(a[2], a[3]), pack2<T>(a[4], a[5]),
-                               pack2<T>(a[6], a[7]));
+    ptx::cp_async_wait_all();  // this thread's own slots only
 #pragma unroll 1
-    for (int q = 0; q < world; ++q)
-      *reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.peers.bufs[q]) + off) = o;
+    for (int i = 0; i < nb; ++i) {
+      const int v = v0 + i * nthreads + tid;
+      if (v >= total) break;
+      float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+      for (int q = 0; q < world; ++q) {
+        float f[8];
+        unpack8<T>(sv[(i * world + q) * nthreads + tid], f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] += f[j];
+      }
+      const uint4 o = make_uint4(pack2<T>(a[0], a[1]), pack2<T>(a[2], a[3]), pack2<T>(a[4], a[5]),
+                                 pack2<T>(a[6], a[7]));
+      const size_t off = offset(v);
+#pragma unroll 1
+      for (int q = 0; q < world; ++q)
+        *reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.peers.bufs[q]) + off) = o;
+    }
   }
 }
 
@@ -1129,7 +1144,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
         ptx::fence_acq_rel_sys();
         allreduce_rows<T>(p, st, tx * C::kTileM + static_cast<int>(rank) * 128, ty,
-                          threadIdx.x - 128, kEpiThreads);
+                          threadIdx.x - 128, kEpiThreads, smem,
+                          C::kChunked ? C::kStageOff : C::kStages * C::kStageBytes);
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
         if (threadIdx.x == 128) {
           __threadfence_system();

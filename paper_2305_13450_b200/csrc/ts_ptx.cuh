@@ -262,6 +262,16 @@ __device__ __forceinline__ int atom_add_release_sys(int* p, int v) {
   return old;
 }
 
+// 16-byte asynchronous global -> shared copy (LDGSTS, L2 only) and its completion wait:
+// many copies in flight per thread without holding registers.
+__device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 // 128-bit load that bypasses L1 (peer data is read once, after a system-scope acquire).
 __device__ __forceinline__ uint4 ld_global_cg_v4(const void* p) {
   uint4 v;
