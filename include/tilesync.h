@@ -114,7 +114,13 @@ typedef enum {
 typedef enum {
   TS_FLAG_KEEP_SEMS = 1,   /* do not zero semaphores at exit (for final-value parity)  */
   TS_FLAG_NO_REORDER = 2,  /* disable "+R": load the dependent A tile before B         */
-  TS_FLAG_NO_WATCHDOG = 4  /* spin forever instead of aborting a wait after ~4 s      */
+  TS_FLAG_NO_WATCHDOG = 4, /* spin forever instead of aborting a wait after ~4 s      */
+  TS_FLAG_ROW_INTERLEAVE = 8 /* fused two-GeMM Row/TileSync chains: claim tiles row by
+                              row across the stages (producer row r, consumer row r,
+                              producer row r+1, ...) instead of stage by stage — for
+                              inputs that arrive row by row (MlpChain.run_host); every
+                              consumer item is still claimed after the producer items
+                              it waits on                                               */
 } ts_flags;
 
 typedef struct {

@@ -24,7 +24,7 @@ TS_DTYPE_F16, TS_DTYPE_BF16 = range(2)
 TS_EPI_NONE, TS_EPI_GELU, TS_EPI_SWIGLU, TS_EPI_RELU = range(4)
 TS_MODE_STREAM, TS_MODE_FUSED = range(2)
 TS_STAGE_GEMM, TS_STAGE_ATTN_DOT, TS_STAGE_CONV2D, TS_STAGE_ALLREDUCE = range(4)
-TS_FLAG_KEEP_SEMS, TS_FLAG_NO_REORDER, TS_FLAG_NO_WATCHDOG = 1, 2, 4
+TS_FLAG_KEEP_SEMS, TS_FLAG_NO_REORDER, TS_FLAG_NO_WATCHDOG, TS_FLAG_ROW_INTERLEAVE = 1, 2, 4, 8
 
 TS_MAX_STAGES = 4
 TS_MAX_DEPS = 4

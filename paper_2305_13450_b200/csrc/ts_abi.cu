@@ -554,6 +554,19 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     ts::StageParams& pw = p->st[dd.producer];
     pw.out_deps[pw.n_out_deps++] = i;
   }
+  if ((d->flags & TS_FLAG_ROW_INTERLEAVE) && d->mode == TS_MODE_FUSED) {
+    const ts::StageParams& s0 = p->st[0];
+    const ts::StageParams& s1 = p->st[1];
+    if (d->n_stages != 2 || d->n_deps != 1 || d->deps[0].producer != 0 ||
+        (d->deps[0].policy != ts::kRow && d->deps[0].policy != ts::kTile) ||
+        s0.kind != ts::kStageGemm || s1.kind != ts::kStageGemm ||
+        s0.order != TS_ORDER_ROW_MAJOR || s1.order != TS_ORDER_ROW_MAJOR ||
+        s0.grid_x != s1.grid_x)
+      return fail(TS_ERR_CONFIG, "row interleaving needs a two-GeMM Row/TileSync chain with "
+                                 "RowMajor orders and equal row tiles");
+    p->il_b1 = s0.grid_y * s0.splits;
+    p->il_b2 = s1.grid_y * s1.splits;
+  }
   // Fused launches run a GeMM-fed dot stage on the last-arriving producer CTA (its
   // tiles leave the claim list); diagnostic flag bit 16 keeps them as claimed items.
   if (d->mode == TS_MODE_FUSED && !((d->flags >> 16) & 1)) {

@@ -125,6 +125,7 @@ struct ChainParams {
   ts_trace_rec* trace;
   int trace_cap;
   int flags;
+  int il_b1, il_b2;    // TS_FLAG_ROW_INTERLEAVE: items per row of stage 0 / 1 (0 = off)
   ts_peer_desc peers;  // kStageAllReduce: the tensor-parallel group
   int ar_done;         // tile halves every rank's owners finalize into this rank's buffer
 };
@@ -183,6 +184,7 @@ struct Cfg {
 };
 
 __device__ __forceinline__ int stage_of(const ChainParams& p, int g) {
+  if (p.il_b1 > 0) return g % (p.il_b1 + p.il_b2) < p.il_b1 ? 0 : 1;
   int s = 0;
 #pragma unroll 1
   while (s + 1 < p.n_stages && g >= p.st[s + 1].item_begin) ++s;
@@ -483,6 +485,11 @@ __device__ __forceinline__ Tile decode(const ChainParams& p, int g) {
   t.s = stage_of(p, g);
   const StageParams& st = p.st[t.s];
   t.tb = g - st.item_begin;
+  if (p.il_b1 > 0) {
+    // row-interleaved claims: row r = [b1 producer items | b2 consumer items]
+    const int per = p.il_b1 + p.il_b2, r = g / per, j = g % per;
+    t.tb = t.s == 0 ? r * p.il_b1 + j : r * p.il_b2 + (j - p.il_b1);
+  }
   order_tile(st.order, st.order_stride, Grid3{st.grid_x, st.grid_y, st.splits}, t.tb, &t.tx,
              &t.ty, &t.tz);
   return t;

@@ -130,6 +130,7 @@ class CuSync:
     num_ctas: int = 0
     extra_flags: int = 0
     swap_ab: bool = False
+    row_interleave: bool = False  # claim tiles row by row across two GeMM stages
     device: torch.device | None = None
     stages: list[CuStage] = field(default_factory=list)
     deps: list[CuDep] = field(default_factory=list)
@@ -392,6 +393,7 @@ class CuSync:
         d.flags = ((0 if self.reorder else _lib.TS_FLAG_NO_REORDER)
                    | (0 if self.watchdog else _lib.TS_FLAG_NO_WATCHDOG)
                    | (_lib.TS_FLAG_KEEP_SEMS if self.keep_sems else 0)
+                   | (_lib.TS_FLAG_ROW_INTERLEAVE if self.row_interleave else 0)
                    | self.extra_flags)
         d.num_ctas = self.num_ctas
         if self._scratch is None:

@@ -17,6 +17,12 @@ w2 = (torch.randn(H, H // 2, device="cuda") / (H // 2) ** 0.5).half()
 xh = x.cpu().pin_memory()
 yh = torch.empty(b, H, dtype=torch.half).pin_memory()
 for name, kw in (("512/512 row", dict(prod_tile_n=512, cons_tile_n=512)),
+                 ("512/512 row interleaved", dict(prod_tile_n=512, cons_tile_n=512, row_interleave=True)),
+                 ("512/512 row z2/1 interleaved", dict(prod_tile_n=512, cons_tile_n=512, prod_splits=2,
+                                                       row_interleave=True)),
+                 ("512/512 row z3/1 interleaved", dict(prod_tile_n=512, cons_tile_n=512, prod_splits=3,
+                                                       row_interleave=True)),
+                 ("256/512 row z2/1 interleaved", dict(cons_tile_n=512, prod_splits=2, row_interleave=True)),
                  ("512/512 row z2/1", dict(prod_tile_n=512, cons_tile_n=512, prod_splits=2)),
                  ("512/512 row z3/1", dict(prod_tile_n=512, cons_tile_n=512, prod_splits=3)),
                  ("cg1 256/256 row z3/1", dict(cta_group=1, prod_splits=3)),

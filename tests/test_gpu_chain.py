@@ -495,3 +495,39 @@ def test_watchdog_on_a_corrupted_semaphore():
     ch()
     torch.cuda.synchronize()
     assert ch.cs.watchdog_fired()
+
+
+@pytest.mark.parametrize("pol,cg,z,pt", [(ts.RowSync(), 2, 1, 512), (ts.TileSync(), 2, 2, 0),
+                                         (ts.RowSync(), 1, 2, 0)])
+def test_row_interleaved_claims(pol, cg, z, pt):
+    """TS_FLAG_ROW_INTERLEAVE (claims row by row across the two stages): the device trace
+    is still dependency-safe under the reference DAG, the final semaphores exact, the
+    result the oracle's, also from pinned host memory (run_host)."""
+    x, w1, w2 = make(600, 1024, 1024, 512, seed=31)
+    ch = ts.MlpChain(x.cuda(), w1.cuda(), w2.cuda(), policy=pol, tile_n=256, cta_group=cg,
+                     prod_splits=z, prod_tile_n=pt, cons_tile_n=pt, keep_sems=True,
+                     row_interleave=True)
+    ch.cs.enable_trace()
+    ch()
+    torch.cuda.synchronize()
+    assert not ch.cs.watchdog_fired()
+    stages, deps = _scenario_dicts(ch.cs)
+    ev_dicts = [{"t": e.time, "stage": e.stage, "tb": e.tb, "kind": e.kind,
+                 "tile": list(e.tile), "k": e.k, "dep": e.dep, "sem": e.sem,
+                 "expected": e.expected} for e in ch.cs.trace_events()]
+    assert O.validate_trace(ev_dicts, stages, deps, fine=True) == []
+    assert {k: tuple(v) for k, v in O.final_semaphores(stages, deps).items()} == \
+        ch.cs.final_semaphores()
+    _, y_ref = oracle_mlp(x, w1, w2, torch.float16)
+    check_close(ch.y, y_ref, torch.float16)
+    e2e = ts.MlpChain(torch.empty_like(x).cuda(), w1.cuda(), w2.cuda(), policy=pol,
+                      tile_n=256, cta_group=cg, prod_splits=z, prod_tile_n=pt,
+                      cons_tile_n=pt, row_interleave=True)
+    xh = x.pin_memory()
+    yh = torch.empty(x.shape[0], w2.shape[0], dtype=x.dtype).pin_memory()
+    for _ in range(3):
+        yh.zero_()
+        e2e.run_host(xh, yh)
+        torch.cuda.synchronize()
+        check_close(yh, y_ref, torch.float16)
+    assert not e2e.cs.watchdog_fired()
