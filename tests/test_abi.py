@@ -170,3 +170,22 @@ def test_allreduce_stage_validation():
     d._keep.bufs[0] = 7 << 20
     with pytest.raises(ConfigError):
         grid_of(d, 2)
+
+
+def test_row_interleave_validation():
+    """TS_FLAG_ROW_INTERLEAVE needs a fused two-GeMM Row/TileSync chain with RowMajor
+    orders and equal row tiles; stream mode ignores it."""
+    d = _desc(cta_group=2)
+    d.flags = _lib.TS_FLAG_ROW_INTERLEAVE
+    assert grid_of(d, 1) == (1, 4)
+    d = _desc(cta_group=1, policy=_lib.TS_POLICY_STRIDED, param=2)
+    d.flags = _lib.TS_FLAG_ROW_INTERLEAVE
+    with pytest.raises(ConfigError):
+        grid_of(d, 1)
+    d = _desc(cta_group=1)
+    d.flags = _lib.TS_FLAG_ROW_INTERLEAVE
+    d.stages[1].order, d.stages[1].order_stride = _lib.TS_ORDER_BANDED_COLUMN_MAJOR, 2
+    with pytest.raises(ConfigError):
+        grid_of(d, 1)
+    d.mode = _lib.TS_MODE_STREAM
+    assert grid_of(d, 1) == (2, 4)
