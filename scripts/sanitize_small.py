@@ -21,5 +21,12 @@ ts.AttentionChain(xa, (torch.randn(768, 512, device=d) / 23).half(),
 xc = torch.randn(1, 14, 14, 128, device=d).half()
 wc = (torch.randn(128, 3, 3, 128, device=d) / 34).half()
 ts.ConvChain(xc, wc, wc.clone(), tile_n=128, cta_group=1)()
+ts.MlpChain(x, w1, w2, policy=ts.RowSync(), tile_n=256, cta_group=2, prod_splits=2,
+            row_interleave=True)()
+from paper_2305_13450_b200 import tp  # noqa: E402
+ar = tp.FusedTPMlp(x, w1, w2, tile_n=256, cta_group=2, cons_splits=2)  # world 1
+tp.connect_group([ar])
+ar()
 torch.cuda.synchronize()
+assert not ar.chain.cs.watchdog_fired()
 print("ok")
