@@ -161,6 +161,13 @@ typedef struct {
                         adds 1 to out_sem[r] after all its rows are stored (system-scope
                         release), so a copy stream can ts_stream_wait for finished rows;
                         never zeroed */
+  int tail_tiles;    /* last-wave balancing (extension): the last `tail_tiles` tiles of this
+                        stage in claim order run as `tail_splits` split-K slices each (the
+                        others unsplit), so the final partial wave spreads over more SMs.
+                        Only for a normal-layout GeMM stage with splits <= 1 that nothing
+                        waits on (no outgoing dependency); workspace / counters sized for
+                        tiles * tail_splits slices. 0 = off */
+  int tail_splits;
 } ts_stage_desc;
 
 typedef enum {

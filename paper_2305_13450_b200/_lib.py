@@ -51,7 +51,7 @@ class StageDesc(ctypes.Structure):
         ("counters", ctypes.c_void_p), ("kind", ctypes.c_int),
         ("conv_n", ctypes.c_int), ("conv_h", ctypes.c_int), ("conv_w", ctypes.c_int),
         ("tile_n", ctypes.c_int), ("in_sem", ctypes.c_void_p), ("in_expected", ctypes.c_int),
-        ("out_sem", ctypes.c_void_p),
+        ("out_sem", ctypes.c_void_p), ("tail_tiles", ctypes.c_int), ("tail_splits", ctypes.c_int),
     ]
 
 

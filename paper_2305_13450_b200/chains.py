@@ -29,7 +29,8 @@ class MlpChain:
                  extra_flags: int = 0, cta_group: int = 2, prod_order: TileOrder = RowMajor(),
                  cons_order: TileOrder = RowMajor(), swap_ab: bool = False,
                  prod_splits: int = 1, cons_splits: int = 1, prod_tile_n: int = 0,
-                 cons_tile_n: int = 0, row_interleave: bool = False):
+                 cons_tile_n: int = 0, row_interleave: bool = False,
+                 cons_tail: tuple = (0, 1)):
         """``row_interleave`` claims GeMM1 row r, GeMM2 row r, GeMM1 row r+1, ... (fused
         RowSync/TileSync, RowMajor orders): for inputs that arrive row by row
         (``run_host``), a row's GeMM2 tiles are not queued behind later rows' GeMM1 tiles
@@ -44,7 +45,7 @@ class MlpChain:
         self.prod = self.cs.stage(x, w1, self.h, epilogue="gelu", order=prod_order, id="gemm1",
                                   splits=prod_splits, tile_n=prod_tile_n)
         self.cons = self.cs.stage(self.h, w2, self.y, order=cons_order, id="gemm2",
-                                  splits=cons_splits, tile_n=cons_tile_n)
+                                  splits=cons_splits, tile_n=cons_tile_n, tail=cons_tail)
         self.dep = self.cs.dependency(policy, self.prod, self.cons, operand="a")
 
     def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:

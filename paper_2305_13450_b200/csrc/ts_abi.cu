@@ -435,8 +435,26 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     sp.order_stride = st.order == TS_ORDER_ROW_MAJOR ? 1 : st.order_stride;
     sp.epilogue = st.epilogue;
     sp.k_blocks = st.k / ts::kBK;
+    sp.tail_tiles = 0;
+    sp.tail_splits = 1;
+    if (st.tail_tiles > 0) {
+      // last-wave balancing; consumers of this stage (checked below) must not exist
+      if (swap || conv || splits > 1 || st.epilogue == TS_EPI_SWIGLU || st.out_sem ||
+          (d->flags & TS_FLAG_ROW_INTERLEAVE))
+        return fail(TS_ERR_CONFIG, "stage %d: tail splitting needs an unsplit normal-layout "
+                                   "GeMM stage (no SwiGLU, row gates or row interleaving)", s);
+      if (st.tail_tiles > sp.grid_x * sp.grid_y || st.tail_splits < 2 ||
+          sp.k_blocks % st.tail_splits)
+        return fail(TS_ERR_CONFIG, "stage %d: tail of %d tiles x %d slices invalid (%d tiles, "
+                                   "%d K-blocks)", s, st.tail_tiles, st.tail_splits,
+                    sp.grid_x * sp.grid_y, sp.k_blocks);
+      if (!st.workspace || !st.counters)
+        return fail(TS_ERR_VALUE, "stage %d: tail slices need workspace and counters", s);
+      sp.tail_tiles = st.tail_tiles;
+      sp.tail_splits = st.tail_splits;
+    }
     sp.item_begin = items;
-    items += sp.grid_x * sp.grid_y * splits;
+    items += sp.grid_x * sp.grid_y * splits + sp.tail_tiles * (sp.tail_splits - 1);
     sp.item_end = items;
     sp.in_dep = -1;
     sp.n_out_deps = 0;
@@ -466,6 +484,8 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       return fail(TS_ERR_CONFIG, "dependency %d: GeMM stages only consume operand A", i);
     const ts::StageParams& ps = p->st[dd.producer];
     ts::StageParams& cs = p->st[dd.consumer];
+    if (ps.tail_tiles > 0)
+      return fail(TS_ERR_CONFIG, "dependency %d: a tail-split stage cannot be waited on", i);
     const ts::Grid3 pg{ps.grid_x, ps.grid_y, ps.splits};
     int r = ts::policy_check(dd.policy, dd.param, pg);
     if (r == ts::kType) return fail(TS_ERR_TYPE, "dependency %d: unknown policy %d", i, dd.policy);

@@ -104,6 +104,9 @@ struct StageParams {
   int in_expected;
   int* out_sem;
   int ar_cols;  // kStageAllReduce: columns of a tile (the producer's tile width)
+  // last-wave balancing: the last tail_tiles tiles (claim order) run as tail_splits
+  // split-K slices each; items = tiles - tail_tiles + tail_tiles * tail_splits
+  int tail_tiles, tail_splits;
 };
 
 struct DepParams {
@@ -464,7 +467,14 @@ __device__ __forceinline__ bool skip_in_gate(const ChainParams& p) { return (p.f
 
 struct Tile {
   int g, s, tb, tx, ty, tz;
+  int z;  // split-K slices of this item's tile (st.splits, or tail_splits for a tail tile)
 };
+
+// Split-K slices of item g of stage st (see StageParams::tail_tiles).
+__device__ __forceinline__ int item_slices(const StageParams& st, int tb) {
+  if (st.tail_tiles > 0 && tb >= st.grid_x * st.grid_y - st.tail_tiles) return st.tail_splits;
+  return st.splits;
+}
 
 // 32 packed 16-bit outputs (64 B) of one row: two 256-bit stores, or four 128-bit ones.
 template <typename T>
@@ -489,6 +499,17 @@ __device__ __forceinline__ Tile decode(const ChainParams& p, int g) {
     // row-interleaved claims: row r = [b1 producer items | b2 consumer items]
     const int per = p.il_b1 + p.il_b2, r = g / per, j = g % per;
     t.tb = t.s == 0 ? r * p.il_b1 + j : r * p.il_b2 + (j - p.il_b1);
+  }
+  t.z = st.splits;
+  const int base = st.grid_x * st.grid_y - st.tail_tiles;
+  if (st.tail_tiles > 0 && t.tb >= base) {
+    // tail tile (base + j / z), slice j % z
+    const int j = t.tb - base;
+    t.z = st.tail_splits;
+    order_tile(st.order, st.order_stride, Grid3{st.grid_x, st.grid_y, 1}, base + j / t.z, &t.tx,
+               &t.ty, &t.tz);
+    t.tz = j % t.z;
+    return t;
   }
   order_tile(st.order, st.order_stride, Grid3{st.grid_x, st.grid_y, st.splits}, t.tb, &t.tx,
              &t.ty, &t.tz);
@@ -713,7 +734,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         const uint64_t pol_a = ah == 1 ? pol_first : (ah == 2 ? pol_normal : pol_last);
         // diagnostic only (flag bit 12): time the chain without semaphore waits
         const bool no_wait = (p.flags >> 12) & 1;
-        const int k_per = st.k_blocks / st.splits;  // K-blocks of this split-K slice
+        const int k_per = st.k_blocks / t.z;  // K-blocks of this split-K slice
         const int kb_begin = t.tz * k_per;
         const int kb_end = kb_begin + k_per;
         // stage.wait() for reference k-step `ks` (policies.py:145-166)
@@ -952,7 +973,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         const StageParams& sp = p.st[stage_of(p, g)];
         if (sp.kind == kStageDot || sp.kind == kStageAllReduce)
           continue;  // no MMA, no accumulator buffer
-        const int kblocks = sp.k_blocks / sp.splits;
+        const int kblocks = sp.k_blocks / item_slices(sp, g - sp.item_begin);
         const int wide = C::kChunked ? sp.wide : 0;
         // instruction descriptor: N = the stage's columns per MMA (chunked stages)
         const uint32_t idesc = C::kChunked ? ptx::idesc_f16(128 * CG, sp.half_n, AbFormat<T>::value)
@@ -1307,7 +1328,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       // full-sector (32-B) stores when the output rows are 32-B aligned
       const bool v8ok = ((reinterpret_cast<uintptr_t>(st.c) | (st.ldc * sizeof(T))) & 31) == 0;
       constexpr int G = C::kEpiGroups;
-      if (st.splits > 1) {
+      if (t.z > 1) {
         // Split-K slice (the reference's z > 1) of a normal tile: publish this CTA's fp32
         // partial rows, count arrivals per (tile, CTA); the last slice to arrive sums all
         // partials, applies the epilogue and stores. Every slice still posts once below
@@ -1318,7 +1339,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         // partial plane of one CTA: [acc_cols / 32 chunks][128 rows][32 floats], so a
         // warp's 32 rows of one chunk are 4 KB contiguous (coalesced writes and reads)
         const size_t plane = static_cast<size_t>(128) * acc_cols;
-        float* mine = st.ws + (static_cast<size_t>(tile_id * st.splits + t.tz) * CG + rank) * plane;
+        float* mine = st.ws + (static_cast<size_t>(tile_id * t.z + t.tz) * CG + rank) * plane;
         const int span = acc_cols / G;
         // only rows < m carry data (small batch: a 128-row tile may hold a single row)
         const int row0 = t.tx * C::kTileM + static_cast<int>(rank) * 128;
@@ -1353,15 +1374,15 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         if (threadIdx.x == 128) {
           const int half_id = tile_id * CG + static_cast<int>(rank);
           const int old = atomicAdd(&st.cnt[half_id], 1);
-          *split_flag = (old == st.splits - 1);
-          if (old == st.splits - 1) st.cnt[half_id] = 0;  // restore the zero invariant
+          *split_flag = (old == t.z - 1);
+          if (old == t.z - 1) st.cnt[half_id] = 0;  // restore the zero invariant
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
         if (*split_flag) {
           ptx::fence_acq_rel_gpu();
           // Reduction, warp-cooperative: one step = 4 rows x 32 columns of one chunk
           // (512 B per slice, lane l: row r0 + l / 8, columns (l % 8) * 4 .. + 4).
-          const float* base = st.ws + static_cast<size_t>(tile_id) * st.splits * CG * plane +
+          const float* base = st.ws + static_cast<size_t>(tile_id) * t.z * CG * plane +
                               static_cast<size_t>(rank) * plane;
           const bool gl = st.epilogue == TS_EPI_GELU;
           const bool rl = st.epilogue == TS_EPI_RELU;
@@ -1385,7 +1406,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
               (p.flags >> 26) & 1 ? ptx::policy_evict_normal() : ptx::policy_evict_first();
           // ~16 float4 loads in flight per lane for the common slice counts (diagnostic
           // flag bit 20 forces the generic loop)
-          const int zsel = (p.flags >> 20) & 1 ? 0 : st.splits;
+          const int zsel = (p.flags >> 20) & 1 ? 0 : t.z;
           if (zsel == 2) {
 #pragma unroll 1
             for (int s0 = warp - 4; s0 < steps; s0 += ss * 8)
@@ -1407,7 +1428,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
 #pragma unroll
             for (int j = 0; j < kSB; ++j) a[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
-            for (int z0 = 0; z0 < st.splits; z0 += 4) {
+            for (int z0 = 0; z0 < t.z; z0 += 4) {
               float4 v[kSB][4];
 #pragma unroll
               for (int j = 0; j < kSB; ++j) {
@@ -1416,7 +1437,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
                     (static_cast<size_t>(sidx / nr4) * 128 + (sidx % nr4) * 4) * 32 + lane * 4;
 #pragma unroll
                 for (int zz = 0; zz < 4; ++zz)
-                  v[j][zz] = (sidx < steps && z0 + zz < st.splits)
+                  v[j][zz] = (sidx < steps && z0 + zz < t.z)
                                  ? __ldcg(reinterpret_cast<const float4*>(base + (z0 + zz) * CG * plane + off))
                                  : make_float4(0.f, 0.f, 0.f, 0.f);
               }

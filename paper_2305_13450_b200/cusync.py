@@ -67,6 +67,7 @@ class CuStage:
     in_sem: torch.Tensor | None = None   # external row gate on operand A (ts_stream_signal)
     out_sem: torch.Tensor | None = None  # per-row "tiles stored" counters (ts_stream_wait)
     tile_n: int = 0     # 0 = the chain's tile_n; 512 = double-width CTA-pair tile
+    tail: tuple = (0, 1)  # (tiles, slices): last-wave balancing of a final stage
 
     @property
     def m(self) -> int:
@@ -171,7 +172,7 @@ class CuSync:
     # -- construction ---------------------------------------------
     def stage(self, a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, epilogue: str = "none",
               order: TileOrder = RowMajor(), id: str | None = None,
-              splits: int = 1, tile_n: int = 0) -> CuStage:
+              splits: int = 1, tile_n: int = 0, tail: tuple = (0, 1)) -> CuStage:
         """Add a GeMM stage. ``splits`` > 1 splits K into that many slices (the
         reference's z extent): each slice posts once, consumers wait for all of them.
         ``tile_n=512`` gives this stage double-width CTA-pair tiles (256 x 512 outputs;
@@ -196,7 +197,14 @@ class CuSync:
         if splits < 1:
             raise ConfigError("splits must be >= 1")
         st = CuStage(self, len(self.stages), id or f"gemm{len(self.stages) + 1}", a, b, c,
-                     epilogue, order, splits, tile_n=tile_n)
+                     epilogue, order, splits, tile_n=tile_n, tail=tuple(tail))
+        if tail[0] > 0:
+            # last-wave balancing (extension): the last tail[0] tiles in claim order run as
+            # tail[1] split-K slices; only for a stage nothing waits on (checked at build)
+            tiles = st.grid.x * st.grid.y
+            st.ws = torch.empty(tiles * tail[1] * self.tile_m * st.width, dtype=torch.float32,
+                                device=a.device)
+            st.cnt = torch.zeros(tiles * self.cta_group, dtype=torch.int32, device=a.device)
         if splits > 1:
             # fp32 partials [tile][slice][tile_m rows][width] and per-(tile, CTA) counters
             tiles = st.grid.x * st.grid.y
@@ -374,6 +382,7 @@ class CuSync:
             sd.in_sem = st.in_sem.data_ptr() if st.in_sem is not None else None
             sd.out_sem = st.out_sem.data_ptr() if st.out_sem is not None else None
             sd.tile_n = st.tile_n
+            sd.tail_tiles, sd.tail_splits = st.tail
             sd.workspace = st.ws.data_ptr() if st.ws is not None else None
             sd.counters = st.cnt.data_ptr() if st.cnt is not None else None
         d.n_deps = len(self.deps)

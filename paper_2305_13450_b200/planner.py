@@ -33,7 +33,7 @@ def _time(fn, iters=10, warm=3) -> float:
     return e0.elapsed_time(e1) * 1e3 / iters
 
 
-def candidates(m: int, mode: str):
+def candidates(m: int, mode: str, n2: int | None = None, units: int = 74):
     """Candidate chain configurations for `m` activation rows.
 
     Large batch: normal tiles (activations on the UMMA M side), CTA pairs or single CTAs,
@@ -78,6 +78,14 @@ def candidates(m: int, mode: str):
             for pol, co, z1 in itertools.product(pols, orders, (2, 3)):
                 out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=cg, cons_order=co,
                                 prod_tile_n=512, cons_tile_n=512, prod_splits=z1))
+            if n2 and n2 % 512 == 0:
+                # last-wave balancing: GeMM2's final partial wave as split-K slices
+                rem = (-(-m // 256) * (n2 // 512)) % units
+                if rem:
+                    for co, z1, zt in itertools.product(orders, (1, 2), (2, 3)):
+                        out.append(dict(policy=RowSync(), mode=mode, tile_n=tn, cta_group=cg,
+                                        cons_order=co, prod_tile_n=512, cons_tile_n=512,
+                                        prod_splits=z1, cons_tail=(rem, zt)))
     return out
 
 
@@ -90,17 +98,21 @@ def describe(kw) -> dict:
         pw = kw.get("prod_tile_n") or kw["tile_n"]
         cw = kw.get("cons_tile_n") or kw["tile_n"]
         tile = f"{m}x{pw}" if pw == cw else f"{m}x{pw}/{m}x{cw}"
-    return {"mode": kw["mode"], "policy": type(kw["policy"]).__name__, "tile": tile,
-            "cta_group": kw["cta_group"], "swap_ab": swap,
-            "splits": [kw.get("prod_splits", 1), kw.get("cons_splits", 1)],
-            "consumer_order": type(co).__name__ + (f"({co.band})" if hasattr(co, "band") else "")}
+    d = {"mode": kw["mode"], "policy": type(kw["policy"]).__name__, "tile": tile,
+         "cta_group": kw["cta_group"], "swap_ab": swap,
+         "splits": [kw.get("prod_splits", 1), kw.get("cons_splits", 1)],
+         "consumer_order": type(co).__name__ + (f"({co.band})" if hasattr(co, "band") else "")}
+    if kw.get("cons_tail", (0, 1))[0]:
+        d["consumer_tail"] = list(kw["cons_tail"])  # (tiles, split-K slices) of the last wave
+    return d
 
 
 def pick_mlp(x, w1, w2, mode="fused"):
     """Time every candidate; return (best kwargs for MlpChain, [(desc, us), ...])."""
     table = []
     best, best_us = None, float("inf")
-    for kw in candidates(x.shape[0], mode):
+    sms = torch.cuda.get_device_properties(x.device).multi_processor_count
+    for kw in candidates(x.shape[0], mode, n2=w2.shape[0], units=sms // 2):
         ch = MlpChain(x, w1, w2, **kw)
         us = _time(ch)
         if ch.cs.watchdog_fired():

@@ -531,3 +531,22 @@ def test_row_interleaved_claims(pol, cg, z, pt):
         torch.cuda.synchronize()
         check_close(yh, y_ref, torch.float16)
     assert not e2e.cs.watchdog_fired()
+
+
+@pytest.mark.parametrize("cg,pt,tail", [(2, 512, (3, 2)), (2, 0, (8, 3)), (1, 0, (1, 4)),
+                                        (2, 512, (6, 4))])
+def test_tail_split_last_stage(cg, pt, tail):
+    """Last-wave balancing (ts_stage_desc.tail_tiles / tail_splits): GeMM2's last tiles in
+    claim order run as split-K slices; the result is the oracle's, relaunches keep the
+    counters at zero."""
+    x, w1, w2 = make(600, 768, 1536, 1024, seed=41)
+    ch = ts.MlpChain(x.cuda(), w1.cuda(), w2.cuda(), tile_n=256, cta_group=cg, prod_tile_n=pt,
+                     cons_tile_n=pt, cons_tail=tail)
+    _, y_ref = oracle_mlp(x, w1, w2, torch.float16)
+    for _ in range(3):
+        ch.y.zero_()
+        ch()
+        torch.cuda.synchronize()
+        check_close(ch.y, y_ref, torch.float16)
+    assert not ch.cs.watchdog_fired()
+    assert int(ch.cons.cnt.abs().sum()) == 0
