@@ -20,4 +20,5 @@ for b in (int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "256").split(",
         _, table = planner.pick_mlp(x, w1, w2, mode)
         for r in sorted(table, key=lambda r: r["us"])[:6]:
             print(f"  {mode:6s} {r['us']:7.1f} us {r['policy']:8s} {r['tile']:22s} cg{r['cta_group']} "
-                  f"z{r['splits'][0]}/{r['splits'][1]} {r['consumer_order']}", flush=True)
+                  f"z{r['splits'][0]}/{r['splits'][1]} {r['consumer_order']} "
+                  f"tail={r.get('consumer_tail', '-')}", flush=True)
