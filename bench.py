@@ -234,7 +234,7 @@ def main():
         base, bcands = planner.pick_mlp(x, w1, w2, mode="stream")
     else:
         fixed = dict(policy=ts.RowSync(), tile_n=256, cta_group=2, prod_tile_n=512,
-                     cons_tile_n=512, prod_splits=2, cons_order=ts.BandedColumnMajor(4))
+                     cons_tile_n=512, cons_tail=(22, 2), cons_order=ts.BandedColumnMajor(4))
         best, cands = dict(fixed, mode="fused"), []
         base, bcands = dict(fixed, mode="stream"), []
     chain = ts.MlpChain(x, w1, w2, **best)

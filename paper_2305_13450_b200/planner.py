@@ -107,10 +107,16 @@ def describe(kw) -> dict:
     return d
 
 
-def pick_mlp(x, w1, w2, mode="fused"):
-    """Time every candidate; return (best kwargs for MlpChain, [(desc, us), ...])."""
+def pick_mlp(x, w1, w2, mode="fused", tie=0.015):
+    """Time every candidate; return (best kwargs for MlpChain, [(desc, us), ...]).
+
+    Large batch: a configuration without GeMM1 split-K slices within `tie` (timing noise)
+    of the fastest is preferred — the slices' second wave re-streams the weights and the
+    partial planes add traffic (ncu: 626 vs 348-359 MB per B=1024 launch,
+    profiles/r01k_traffic.txt), which costs power under the cap for no measured gain."""
     table = []
     best, best_us = None, float("inf")
+    timed = []
     sms = torch.cuda.get_device_properties(x.device).multi_processor_count
     for kw in candidates(x.shape[0], mode, n2=w2.shape[0], units=sms // 2):
         ch = MlpChain(x, w1, w2, **kw)
@@ -118,8 +124,15 @@ def pick_mlp(x, w1, w2, mode="fused"):
         if ch.cs.watchdog_fired():
             continue
         table.append({**describe(kw), "us": us})
+        timed.append((us, kw))
         if us < best_us:
             best, best_us = kw, us
+    if x.shape[0] >= 512 and best is not None and best.get("prod_splits", 1) > 1:
+        lean = [(us, kw) for us, kw in timed
+                if kw.get("prod_splits", 1) == 1 and not kw.get("swap_ab", False)
+                and us <= best_us * (1 + tie)]
+        if lean:
+            best = min(lean, key=lambda t: t[0])[1]
     return best, table
 
 
