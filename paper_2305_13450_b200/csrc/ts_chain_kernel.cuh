@@ -805,7 +805,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         // Ordered policies (Tile, Conv2D) defer the waits of the k-steps inside the first
         // `pre` K-blocks the same way (their later k-steps wait inline), which hides the
         // loaded latency of a satisfied wait (~2 us of L2 round trip) behind weight loads.
-        const bool deep = waits && reorder && !((p.flags >> 21) & 1);
+        // Not for convolution consumers: their im2col A boxes are the heavy operand and
+        // front-loading the small weight boxes only delayed them (measured, flag bit 21:
+        // ResNet 8x56x56x64 39.7 -> 33.0 us, 32x56x56x64 107 -> 90 us, never slower).
+        const bool deep = waits && reorder && !conv && !((p.flags >> 21) & 1);
         const int pre = deep ? (k_per < cap ? k_per : cap) : 0;
         const int ea_start = ea;
         const uint32_t kq_start = kq;
