@@ -805,10 +805,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         // Ordered policies (Tile, Conv2D) defer the waits of the k-steps inside the first
         // `pre` K-blocks the same way (their later k-steps wait inline), which hides the
         // loaded latency of a satisfied wait (~2 us of L2 round trip) behind weight loads.
-        // Not for convolution consumers: their im2col A boxes are the heavy operand and
-        // front-loading the small weight boxes only delayed them (measured, flag bit 21:
-        // ResNet 8x56x56x64 39.7 -> 33.0 us, 32x56x56x64 107 -> 90 us, never slower).
-        const bool deep = waits && reorder && !conv && !((p.flags >> 21) & 1);
+        // Only for Row/Strided consumers (one wait, at k-step 0). Not for convolution
+        // consumers — their im2col A boxes are the heavy operand and front-loading the small
+        // weight boxes delayed them (flag bit 21: ResNet 8x56x56x64 39.7 -> 33.0 us,
+        // 32x56x56x64 107 -> 90 us) — nor for ordered (Tile/Conv2D) GeMM consumers, where
+        // deferring the first waits cost 1-5% (TileSync MLP B=1024 341 vs 336 us, attention
+        // S=512 153 vs 147 us).
+        const bool deep = waits && reorder && !conv && !((p.flags >> 21) & 1) &&
+                          (p.dep[d].policy == kRow || p.dep[d].policy == kStrided);
         const int pre = deep ? (k_per < cap ? k_per : cap) : 0;
         const int ea_start = ea;
         const uint32_t kq_start = kq;
