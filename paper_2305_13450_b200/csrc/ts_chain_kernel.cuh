@@ -57,10 +57,13 @@ constexpr int kStageDot = 1;   // attention's fused softmax-dot over QKV column 
 constexpr int kStageAllReduce = 3;  // TP all-reduce of the producer's tiles over peer memory
 constexpr int kStageConv = 2;  // 3x3 "same" Conv2D as implicit GeMM (im2col TMA A operand)
 
-// K-blocks per tcgen05.commit (flags bits 17-18: 1 -> 1, 2 -> 2, 3 -> 4; 0 -> default 2).
+// K-blocks per tcgen05.commit (flags bits 17-18: 1 -> 1, 2 -> 2, 3 -> 4; 0 -> default 1).
+// One commit per K-block frees ring entries soonest; measured against 2 (scripts/flag_ab.py
+// 17): equal or 1-3% faster on every chain (MLP B=256 146.5 -> 142.2 us, B=1024 headline
+// 292 -> 286 us, attention S=512 147 -> 144.5 us); 4 per commit is 30% slower.
 __host__ __device__ __forceinline__ int commit_group(int flags) {
   const int g = (flags >> 17) & 3;
-  return g ? 1 << (g - 1) : 2;
+  return g ? 1 << (g - 1) : 1;
 }
 // Ring-entry counter step without a division.
 __device__ __forceinline__ int wrap_inc(int e, int n) { return e + 1 == n ? 0 : e + 1; }
