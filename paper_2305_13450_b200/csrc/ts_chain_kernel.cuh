@@ -181,7 +181,7 @@ struct Cfg {
   static constexpr int kBarOffset =
       kChunked ? kStageOff + (kEpiThreads / 32) * 4096 : kStages * kStageBytes;
   // K-block full, commit-group empty; tmem full/empty x2; tile ring full/empty; peer_done
-  static constexpr int kNumBars = kFullRing + kCommitRing + 4 + 2 * kTileRing + kPeerRing;
+  static constexpr int kNumBars = kFullRing + kCommitRing + 4 + 2 * kTileRing + kPeerRing + 2;
   // + tile ring ids, TMEM slot, flags and the last-arriver dot list (64 ints), ring-entry
   // owners (commit group that last read each entry)
   static constexpr int kSmemBytes = 1024 + kBarOffset + kNumBars * 8 + 64 + 272 + 4 * kRing;
@@ -597,7 +597,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
   uint64_t* ti_full = tmem_empty + 2;
   uint64_t* ti_empty = ti_full + kTileRing;
   uint64_t* peer_done = ti_empty + kTileRing;
-  int* ti_item = reinterpret_cast<int*>(peer_done + kPeerRing);
+  uint64_t* dot_msg = peer_done + kPeerRing;  // peer CTA: leader's list of released dot tiles
+  uint64_t* dot_done = dot_msg + 1;           // leader: peer finished its half of them
+  int* ti_item = reinterpret_cast<int*>(dot_done + 1);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ti_item + kTileRing);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   int* split_flag = last_flag + 1;
@@ -619,6 +621,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       ptx::mbar_init(&tmem_empty[i], CG * kEpiWarps);
     }
     for (int i = 0; i < kPeerRing; ++i) ptx::mbar_init(&peer_done[i], 1);
+    ptx::mbar_init(dot_msg, 1);
+    ptx::mbar_init(dot_done, 1);
     for (int i = 0; i < kTileRing; ++i) {
       ptx::mbar_init(&ti_full[i], 1);
       // leader MMA warp + every epilogue warp of the pair + the peer's producer lane
@@ -1128,21 +1132,28 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
     }
     // Compute dot tile (tx, ty) of stage ds with the 128 epilogue threads (its wait is
     // already satisfied), then post to its consumers (thread 128).
-    auto run_dot = [&](int ds, int tx, int ty, int tb) {
+    // Compute dot tile (tx, ty) — all its rows (half < 0) or one CTA's 128 of a pair's 256
+    // (half 0 / 1) — and, if `post`, post it to its consumers (thread 128).
+    auto run_dot_rows = [&](int ds, int tx, int ty, int tb, int half) {
       const StageParams& sd = p.st[ds];
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
       ptx::fence_acq_rel_gpu();
-      if (threadIdx.x == 128) trace_event(p, ptx::global_timer(), 7, ds, tb, -1, -1, -1, -1, tx, ty);
+      if (threadIdx.x == 128 && half <= 0)
+        trace_event(p, ptx::global_timer(), 7, ds, tb, -1, -1, -1, -1, tx, ty);
       // a dot tile covers BN / 128 heads (the paper's stride H / (8 Ty));
       // one warp per (row, head), warps striding over the tile's rows x heads
       constexpr int kHeads = BN >= 128 ? BN / 128 : 1;
-      const int items = C::kTileM * kHeads;
+      const int items = (half < 0 ? C::kTileM : 128) * kHeads;
+      const int row0 = tx * C::kTileM + (half > 0 ? 128 : 0);
       // loads in flight per warp: 2 x kB items (fewer for 384-thread CTAs, 168 registers)
       constexpr int kB = C::kChunked ? 2 : 4;
 #pragma unroll 1
       for (int it0 = (warp - 4) * 2; it0 < items; it0 += kEpiWarps * 2 * kB)
-        dot_batch_warp<T, kB>(sd, tx * C::kTileM, kHeads, it0, kEpiWarps * 2, items, ty * kHeads, lane);
+        dot_batch_warp<T, kB>(sd, row0, kHeads, it0, kEpiWarps * 2, items, ty * kHeads, lane);
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+    };
+    auto post_dot = [&](int ds, int tx, int ty, int tb) {
+      const StageParams& sd = p.st[ds];
       if (threadIdx.x == 128) {
         const uint64_t tnow = ptx::global_timer();
         trace_event(p, tnow, 8, ds, tb, -1, -1, -1, -1, tx, ty);
@@ -1159,6 +1170,13 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         trace_event(p, tnow, 4, ds, tb, -1, -1, -1, -1, tx, ty);
       }
     };
+    auto run_dot = [&](int ds, int tx, int ty, int tb) {
+      run_dot_rows(ds, tx, ty, tb, -1);
+      post_dot(ds, tx, ty, tb);
+    };
+    // last-arriver dot tiles split over a CTA pair (diagnostic flag bit 28: leader only)
+    const bool dsplit = CG == 2 && !((p.flags >> 28) & 1);
+    uint32_t dmsg = 0, ddone = 0;  // dot_msg / dot_done phases (peer / leader)
 #pragma unroll 1
     for (int it = 0;; ++it) {
       const int g = ring_take(it, CG == 2 && !leader);
@@ -1582,6 +1600,16 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
                   }
                 }
                 *dot_count = n;
+                if (dsplit) {
+                  // hand the list to the peer CTA, which computes the lower 128 rows
+                  for (int i = 0; i < n; ++i) {
+                    ptx::st_cluster_u32(ptx::mapa(&dot_list[i], 1), static_cast<uint32_t>(dot_list[i]));
+                    ptx::st_cluster_u32(ptx::mapa(&dot_list[32 + i], 1),
+                                        static_cast<uint32_t>(dot_list[32 + i]));
+                  }
+                  ptx::st_cluster_u32(ptx::mapa(dot_count, 1), static_cast<uint32_t>(n));
+                  ptx::mbar_arrive_remote(ptx::mapa(dot_msg, 1));
+                }
               }
             }
           }
@@ -1594,14 +1622,31 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           trace_event(p, tnow, 4, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
         }
       }
-      if (st.dot_dep >= 0 && leader) {
-        // last-arriver dot tiles released by this tile's posts
+      if (st.dot_dep >= 0 && (leader || dsplit)) {
+        // last-arriver dot tiles released by this tile's posts; split over a CTA pair the
+        // leader computes rows [0, 128) of each and the peer (told by the leader's list)
+        // rows [128, 256), and the leader posts once the peer's rows are stored
+        if (!leader) {
+          ptx::mbar_wait_cluster(dot_msg, dmsg & 1);
+          ++dmsg;
+        }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
         const int n = *dot_count;
         const int ds = p.dep[st.dot_dep].consumer;
-        for (int i = 0; i < n; ++i) run_dot(ds, t.tx, dot_list[i], dot_list[32 + i]);
+        const int half = dsplit ? (leader ? 0 : 1) : -1;
+        for (int i = 0; i < n; ++i) run_dot_rows(ds, t.tx, dot_list[i], dot_list[32 + i], half);
+        if (leader) {
+          if (dsplit && n > 0) {
+            if (threadIdx.x == 128) ptx::mbar_wait_cluster(dot_done, ddone & 1);
+            ++ddone;
+          }
+          for (int i = 0; i < n; ++i) post_dot(ds, t.tx, dot_list[i], dot_list[32 + i]);
+        } else if (n > 0 && threadIdx.x == 128) {
+          __threadfence();
+          ptx::mbar_arrive_remote(ptx::mapa(dot_done, 0));
+        }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-        if (threadIdx.x == 128) *dot_count = 0;
+        if (leader && threadIdx.x == 128) *dot_count = 0;
       }
       ++local;
       u += 1 + wide;
