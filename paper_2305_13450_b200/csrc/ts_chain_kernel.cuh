@@ -658,8 +658,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
     } else {
       ptx::mbar_wait(&ti_full[slot], (it / kTileRing) & 1);
     }
-    const int g = ti_item[slot];
-    __syncwarp();
+    // lane 0 reads the id and is the lane that releases the slot; the others get it by
+    // shuffle (so no lane's shared-memory read is ordered only through another's arrive)
+    int g = lane == 0 ? ti_item[slot] : 0;
+    g = __shfl_sync(0xffffffffu, g, 0);
     if (lane == 0) {
       if (remote_release) {
         ptx::mbar_arrive_remote(ptx::mapa(&ti_empty[slot], 0));
