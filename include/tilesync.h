@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 4
+#define TS_ABI_VERSION 5
 
 /* ---- status codes ---------------------------------------------------------------- */
 typedef enum {
@@ -101,7 +101,7 @@ typedef enum { TS_DTYPE_F16 = 0, TS_DTYPE_BF16 = 1 } ts_dtype;
 
 typedef enum {
   TS_EPI_NONE = 0,   /* C = A x B^T                                        */
-  TS_EPI_GELU = 1,   /* C = GeLU_erf(A x B^T)   */
+  TS_EPI_GELU = 1,   /* C = GeLU_tanh(A x B^T) (GPT-3 tanh form) */
   TS_EPI_SWIGLU = 2, /* C = SiLU(gate) * up, gate/up interleaved per tile  */
   TS_EPI_RELU = 3    /* C = max(A x B^T, 0) (conv layers, BN folded)      */
 } ts_epilogue;
@@ -201,10 +201,15 @@ typedef struct {
   int world, rank;             /* group size (1..TS_MAX_PEERS) and this rank             */
   void* bufs[TS_MAX_PEERS];    /* rank q's allreduce buffer (its stage c)                */
   int* sems[TS_MAX_PEERS];     /* rank q's semaphores of the producer -> allreduce dep   */
-  int* done[TS_MAX_PEERS];     /* rank q's arrival counter (int32, zero on entry; kept
-                                  zero): each owner CTA adds 1 per tile it finalized into
-                                  rank q's buffer; rank q's kernel exits once it counts
-                                  every tile (x cta_group) and resets it                 */
+  int* done[TS_MAX_PEERS];     /* rank q's arrival counter (int32, zero before the first
+                                  launch): each owner CTA adds 1 per tile half it
+                                  finalized into rank q's buffer; rank q's kernel exits
+                                  once it reaches epoch x tiles x cta_group              */
+  int epoch;                   /* launch generation, >= 1, advanced by 1 per launch on
+                                  every rank in lockstep. The producer -> all-reduce
+                                  semaphores and the done counters are monotone (never
+                                  reset by the kernel): launch e waits for e x count, so a
+                                  peer's state from launch e-1 never satisfies a wait    */
 } ts_peer_desc;
 
 typedef struct {

@@ -67,7 +67,7 @@ class PeerDesc(ctypes.Structure):
     _fields_ = [
         ("world", ctypes.c_int), ("rank", ctypes.c_int),
         ("bufs", ctypes.c_void_p * TS_MAX_PEERS), ("sems", ctypes.c_void_p * TS_MAX_PEERS),
-        ("done", ctypes.c_void_p * TS_MAX_PEERS),
+        ("done", ctypes.c_void_p * TS_MAX_PEERS), ("epoch", ctypes.c_int),
     ]
 
 
@@ -130,7 +130,7 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.ts_abi_version() != 4:
+    if lib.ts_abi_version() != 5:
         raise RuntimeError("libtilesync_b200.so ABI version mismatch")
     _lib = lib
     return lib

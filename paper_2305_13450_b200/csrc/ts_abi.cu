@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -131,13 +132,20 @@ int sm_count() {
 template <int BN, int CG, typename T, bool SW = false>
 int launch_one(const ts::ChainParams& p, int units, cudaStream_t stream) {
   using C = ts::Cfg<BN, CG, SW>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(ts::chain_kernel<BN, CG, T, SW>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
+  // the dynamic shared-memory opt-in is a per-device function attribute: set it once for
+  // every device this instantiation launches on (the caller's current device)
+  constexpr int kMaxDev = 64;
+  static std::atomic<int> attr_set[kMaxDev];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= kMaxDev) return fail(TS_ERR_CUDA, "device ordinal %d unsupported", dev);
+  if (attr_set[dev].load(std::memory_order_acquire) == 0) {
+    e = cudaFuncSetAttribute(ts::chain_kernel<BN, CG, T, SW>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    attr_set[dev].store(1, std::memory_order_release);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG, 1, 1);
   cfg.blockDim = dim3(C::kThreads, 1, 1);
@@ -150,7 +158,7 @@ int launch_one(const ts::ChainParams& p, int units, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, ts::chain_kernel<BN, CG, T, SW>, p);
+  e = cudaLaunchKernelEx(&cfg, ts::chain_kernel<BN, CG, T, SW>, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "chain_kernel launch");
   return TS_OK;
@@ -309,6 +317,11 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
           return fail(TS_ERR_VALUE, "stage %d: peer %d has a null or misaligned pointer", s, q);
       if (pr->bufs[pr->rank] != st.c)
         return fail(TS_ERR_VALUE, "stage %d: peers.bufs[rank] must be this stage's c", s);
+      if (pr->epoch < 1) return fail(TS_ERR_VALUE, "stage %d: peers.epoch must be >= 1", s);
+      // The epilogue stages peer vectors in the operand ring, which is idle only when no
+      // GeMM item follows; a second all-reduce stage would share p->peers / p->ar_done.
+      if (s != d->n_stages - 1)
+        return fail(TS_ERR_CONFIG, "stage %d: the allreduce stage must be the chain's last stage", s);
       if (swap) return fail(TS_ERR_CONFIG, "stage %d: the allreduce stage needs normal tiles", s);
       int prod = -1;
       for (int i = 0; i < d->n_deps; ++i)
@@ -793,6 +806,7 @@ int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
     q.item_lo = q.st[i].item_begin;
     q.item_hi = q.st[i].item_end;
     const int n = q.item_hi - q.item_lo;
+    if (n <= 0) continue;  // e.g. a rank that owns no all-reduce tile
     r = launch_dispatch(bn, cg, desc->swap_ab, dtype, q, ctas < n ? ctas : n, s);
     if (r) return r;
   }

@@ -1204,8 +1204,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         const int tx = lin / st.grid_y, ty = lin % st.grid_y;
         const DepParams& dp = p.dep[st.in_dep];
         if (threadIdx.x == 128) {
+          // the group's semaphores are monotone across launches (epoch scheme): launch e
+          // waits for e x pgz posts, so a peer's value from launch e-1 never satisfies it
           const int idx = post_target(dp.policy, dp.param, tx, ty, Grid3{dp.pgx, dp.pgy, dp.pgz});
-          for (int q = 0; q < world; ++q) sem_spin_sys(p, p.peers.sems[q] + idx, dp.pgz);
+          for (int q = 0; q < world; ++q)
+            sem_spin_sys(p, p.peers.sems[q] + idx, dp.pgz * p.peers.epoch);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
         ptx::fence_acq_rel_sys();
@@ -1682,26 +1685,22 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
   __syncthreads();
   if (*last_flag) {
     __threadfence();
-    // All-reduce stage in this launch: every owner (on every rank) has finalized its
-    // tiles into this rank's buffer once the done counter is complete — and has then
-    // finished reading this rank's semaphores, so they may be reset below.
+    // All-reduce stage in this launch: this rank's buffer is final once every owner (on
+    // every rank) has counted its tiles into the done counter. The counter and the
+    // producer -> all-reduce semaphores are monotone (epoch e waits for e x count) and
+    // never reset here: a reset could race with a faster peer's next launch reading them.
     bool ar_here = false;
     for (int s = 0; s < p.n_stages; ++s)
       if (p.st[s].kind == kStageAllReduce && p.st[s].item_begin >= p.item_lo &&
           p.st[s].item_end <= p.item_hi)
         ar_here = true;
     if (ar_here) {
-      if (threadIdx.x == 0) {
-        sem_spin_sys(p, p.peers.done[p.peers.rank], p.ar_done);
-        *p.peers.done[p.peers.rank] = 0;
-      }
+      if (threadIdx.x == 0) sem_spin_sys(p, p.peers.done[p.peers.rank], p.ar_done * p.peers.epoch);
       __syncthreads();
     }
     if ((p.flags & TS_FLAG_KEEP_SEMS) == 0) {
       for (int d = 0; d < p.n_deps; ++d) {
-        // a dependency read from peer GPUs is reset only by the launch that ran its
-        // all-reduce consumer (stream mode launches stages one by one)
-        if (p.st[p.dep[d].consumer].kind == kStageAllReduce && !ar_here) continue;
+        if (p.st[p.dep[d].consumer].kind == kStageAllReduce) continue;  // epoch-monotone
         for (int i = threadIdx.x; i < p.dep[d].sem_n; i += C::kThreads) p.dep[d].sem[i] = 0;
       }
     }

@@ -160,6 +160,14 @@ class CuSync:
         swapped."""
         return self.tile_n if self.swap_ab else BM * self.cta_group
 
+    def _check_open(self) -> None:
+        """Stages may not follow an all-reduce stage: it stages peer vectors in the
+        operand ring, which is idle only when no GeMM item comes after it."""
+        if len(self.stages) >= _lib.TS_MAX_STAGES:
+            raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
+        if any(st.kind == "allreduce" for st in self.stages):
+            raise ConfigError("the all-reduce stage must be the chain's last stage")
+
     def _check_tile_n(self, tile_n: int) -> None:
         """Per-stage tile width: 0 (the chain's), or 384 / 512 (two MMAs of 192 / 256
         columns per K-block) on cta_group=2, tile_n=256 chains."""
@@ -178,8 +186,7 @@ class CuSync:
         ``tile_n=512`` gives this stage double-width CTA-pair tiles (256 x 512 outputs;
         chains with ``cta_group=2, tile_n=256`` only)."""
         self._check_tile_n(tile_n)
-        if len(self.stages) >= _lib.TS_MAX_STAGES:
-            raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
+        self._check_open()
         if epilogue not in _EPI:
             raise ConfigError(f"unknown epilogue {epilogue!r}")
         for t, name in ((a, "a"), (b, "b"), (c, "c")):
@@ -222,8 +229,7 @@ class CuSync:
         Dropout(Softmax(XQ . XV)) . XK per 128-column head, with ``qkv`` [m, 3n] holding
         [Q heads | K heads | V heads]. Column-tile local, as its StridedSync dependency
         defines it; dropout p = 0 (inference)."""
-        if len(self.stages) >= _lib.TS_MAX_STAGES:
-            raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
+        self._check_open()
         for t, name in ((qkv, "qkv"), (out, "out")):
             if t.dim() != 2 or t.stride(1) != 1 or t.dtype not in _DT or not t.is_cuda:
                 raise ValueError(f"{name} must be a row-major fp16/bf16 CUDA matrix")
@@ -244,8 +250,7 @@ class CuSync:
         ``out`` NHWC [N, H, W, Cout]. Output rows are the N*H*W pixels, columns the output
         channels; the A operand is gathered by an im2col TMA map (zero padding at the
         image border). Feed it from another stage with ``Conv2DTileSync(9)``."""
-        if len(self.stages) >= _lib.TS_MAX_STAGES:
-            raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
+        self._check_open()
         if epilogue not in ("none", "relu", "gelu"):
             raise ConfigError(f"unsupported conv epilogue {epilogue!r}")
         if x.dim() != 4 or out.dim() != 4 or w.dim() != 4 or tuple(w.shape[1:3]) != (3, 3):
@@ -288,6 +293,8 @@ class CuSync:
             raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
         if producer.kind != "gemm" or producer.epilogue == "swiglu" or self.swap_ab:
             raise ConfigError("the all-reduce stage sums a normal-layout GeMM stage's output")
+        if any(st.kind == "allreduce" for st in self.stages):
+            raise ConfigError("a chain has at most one all-reduce stage")
         c = producer.c
         st = CuStage(self, len(self.stages), id or "allreduce", c, c, c, "none", RowMajor(),
                      kind="allreduce", tile_n=producer.tile_n)
@@ -299,8 +306,14 @@ class CuSync:
 
     @property
     def allreduce_done(self) -> torch.Tensor:
-        """This rank's all-reduce arrival counter (zero between launches)."""
+        """This rank's all-reduce arrival counter (epoch x tiles x cta_group after the
+        epoch-th launch)."""
         return self._ar_done
+
+    @property
+    def epoch(self) -> int:
+        """Launches of the all-reduce group so far (0 before the first)."""
+        return 0 if self._peers is None else int(self._peers.epoch)
 
     def allreduce_dep(self) -> "CuDep":
         return next(d for d in self.deps if d.consumer.kind == "allreduce")
@@ -320,6 +333,9 @@ class CuSync:
         pd.world, pd.rank = world, rank
         for q in range(world):
             pd.bufs[q], pd.sems[q], pd.done[q] = ptr(bufs[q]), ptr(sems[q]), ptr(dones[q])
+        # launch generation: the group's all-reduce semaphores and done counters are
+        # monotone (zero now); every rank advances the epoch once per launch in lockstep
+        pd.epoch = 0
         self._peers = pd
         self._desc = None
 
@@ -436,10 +452,14 @@ class CuSync:
                 self._desc.trace = self._trace.data_ptr()
                 self._desc.trace_cap = self._trace_cap
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        if self._trace is not None:
-            self._scratch[2].zero_()
-        _lib.check(_lib.load().ts_chain_launch(ctypes.byref(self._desc),
-                                               ctypes.c_void_p(s.cuda_stream)))
+        if self._peers is not None:
+            self._peers.epoch += 1  # ts_chain_launch copies the peer descriptor
+        # the library launches on (and sizes the grid for) the caller's current device
+        with torch.cuda.device(self.device):
+            if self._trace is not None:
+                self._scratch[2].zero_()
+            _lib.check(_lib.load().ts_chain_launch(ctypes.byref(self._desc),
+                                                   ctypes.c_void_p(s.cuda_stream)))
 
     __call__ = launch
 

@@ -33,6 +33,13 @@ def _time(fn, iters=10, warm=3) -> float:
     return e0.elapsed_time(e1) * 1e3 / iters
 
 
+def _check_watchdog(ch, kw) -> None:
+    """A fired semaphore watchdog is a deadlock or a protocol bug, never a slow
+    candidate: fail loudly (the device analogue of detect_deadlock, engine.py:614-637)."""
+    if ch.cs.watchdog_fired():
+        raise RuntimeError(f"semaphore watchdog fired while timing candidate {kw}")
+
+
 def candidates(m: int, mode: str, n2: int | None = None, units: int = 74):
     """Candidate chain configurations for `m` activation rows.
 
@@ -121,8 +128,7 @@ def pick_mlp(x, w1, w2, mode="fused", tie=0.015):
     for kw in candidates(x.shape[0], mode, n2=w2.shape[0], units=sms // 2):
         ch = MlpChain(x, w1, w2, **kw)
         us = _time(ch)
-        if ch.cs.watchdog_fired():
-            continue
+        _check_watchdog(ch, kw)
         table.append({**describe(kw), "us": us})
         timed.append((us, kw))
         if us < best_us:
@@ -246,8 +252,7 @@ def sweep_conv(batches=(1, 8, 32, 128, 256), layers=RESNET38_LAYERS, device=None
                 for kw in conv_candidates(c, mode, b * hw * hw):
                     ch = ConvChain(x, w1, w2, **kw)
                     us = _time(ch, iters=20)
-                    if ch.cs.watchdog_fired():
-                        continue
+                    _check_watchdog(ch, kw)
                     if mode not in best or us < best[mode][0]:
                         best[mode] = (us, kw)
             xt = x.permute(0, 3, 1, 2)  # NCHW view of NHWC memory = channels_last
@@ -294,8 +299,7 @@ def sweep_swiglu(batches=(256, 1024, 2048), tps=(8, 1), hidden=4096, ffn=14336, 
                     except Exception:  # shapes a width does not divide
                         continue
                     us = _time(ch, iters=20)
-                    if ch.cs.watchdog_fired():
-                        continue
+                    _check_watchdog(ch, {"tile": (pw, cw), "policy": pol, "mode": mode})
                     if us < best.get(mode, (float("inf"),))[0]:
                         best[mode] = (us, {"policy": type(pol).__name__,
                                            "tile": f"256x{pw}/256x{cw or 256}"})

@@ -129,7 +129,8 @@ def order(s):
 
 
 def main():
-    """argv: B then variants MODE:POLICY:PROD_ORDER:CONS_ORDER, e.g. fused:row:row:band4"""
+    """argv: B then variants MODE:POLICY:PROD_ORDER:CONS_ORDER[:FLAGS:SWAP_TN:Z1/Z2:W1/W2:TAIL],
+    e.g. fused:row:row:band4 or fused:row:row:band4:0:0:1/1:512/512:22,3"""
     b = int(sys.argv[1])
     variants = sys.argv[2:] or ["stream:row:row:row", "fused:row:row:row"]
     torch.manual_seed(0)
@@ -144,8 +145,9 @@ def main():
         zs = [int(z) for z in parts[6].split("/")] if len(parts) > 6 else [1]
         z1, z2 = zs[0], (zs[1] if len(zs) > 1 else 1)
         widths = [int(w) for w in parts[7].split("/")] if len(parts) > 7 else [0, 0]
+        tail = tuple(int(t) for t in parts[8].split(",")) if len(parts) > 8 else (0, 1)
         policy = {"row": ts.RowSync(), "tile": ts.TileSync()}[pol]
-        kw = dict(prod_splits=z1, cons_splits=z2)
+        kw = dict(prod_splits=z1, cons_splits=z2, cons_tail=tail)
         kw.update(dict(swap_ab=True, tile_n=swap_tn) if swap_tn else
                   dict(prod_tile_n=widths[0], cons_tile_n=widths[1]))
         ch = ts.MlpChain(x, w1, w2, policy=policy, mode=mode, prod_order=order(po),

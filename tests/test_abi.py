@@ -35,7 +35,7 @@ def test_every_declared_symbol_is_exported():
 
 
 def test_abi_version():
-    assert _lib.load().ts_abi_version() == 4
+    assert _lib.load().ts_abi_version() == 5
 
 
 def test_struct_layout_matches_header(tmp_path):
@@ -139,7 +139,7 @@ def _allreduce_desc(world=2, rank=0, policy=_lib.TS_POLICY_TILE):
     dep.producer, dep.consumer, dep.operand, dep.policy, dep.param = 1, 2, 0, policy, 0
     dep.sem = 3 << 20
     pd = _lib.PeerDesc()
-    pd.world, pd.rank = world, rank
+    pd.world, pd.rank, pd.epoch = world, rank, 1
     for q in range(world):
         pd.bufs[q] = y if q == rank else (4 + q) << 20
         pd.sems[q] = dep.sem if q == rank else (12 + q) << 20
@@ -168,6 +168,15 @@ def test_allreduce_stage_validation():
     d = _allreduce_desc()
     d.stages[2].c = d.stages[2].a = 7 << 20  # sums its producer's output in place
     d._keep.bufs[0] = 7 << 20
+    with pytest.raises(ConfigError):
+        grid_of(d, 2)
+    d = _allreduce_desc()
+    d._keep.epoch = 0  # launch generations start at 1 (monotone semaphores)
+    with pytest.raises(ValueError):
+        grid_of(d, 2)
+    d = _allreduce_desc()  # no stage may follow the all-reduce (it borrows the smem ring)
+    d.n_stages = 4
+    d.stages[3] = d.stages[1]
     with pytest.raises(ConfigError):
         grid_of(d, 2)
 

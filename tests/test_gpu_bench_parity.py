@@ -1,0 +1,192 @@
+"""Device parity at the BASELINE.json sizes, for the configurations bench.py and the planner
+actually run (VERDICT r01 "what's weak" #1).
+
+For each case the chain is built exactly as the benchmark builds it (the planner's pick
+on this device, plus fixed plans covering the headline 256x512 + BandedColumnMajor(4) +
+GeMM2-tail configuration and the split-K small-batch plans) and checked two ways:
+
+* numerics: the output against the CPU oracle (oracle/tilesync_oracle.py, fp32 over the
+  same fp16/bf16-rounded inputs, intermediate rounded to the storage dtype) within the
+  stated tolerance |dev - oracle| <= ATOL + RTOL |oracle| (fp16: 2e-2 + 1e-2, bf16: 6e-2 +
+  3e-2);
+* synchronization: the device's final semaphore values (``keep_sems=True``) against the
+  reference simulator's for the same tile grids (tests/golden/bench_scenarios.json, made
+  by tests/golden/make_bench_golden.py from /root/reference), bit for bit.
+
+Inputs are seeded per size and shared between plans; the oracle result is cached per size.
+"""
+
+import functools
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2305_13450_b200 as ts
+from conftest import GOLDEN
+from oracle import tilesync_oracle as O
+from paper_2305_13450_b200 import planner
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float16: (2e-2, 1e-2), torch.bfloat16: (6e-2, 3e-2)}
+DT = {torch.float16: "fp16", torch.bfloat16: "bf16"}
+H, FFN = 12288, 6144
+GOLD = {r["key"]: r for r in json.loads((GOLDEN / "bench_scenarios.json").read_text())}
+KINDS = {ts.TileSync: "tile", ts.RowSync: "row", ts.StridedSync: "strided",
+         ts.Conv2DTileSync: "conv2d"}
+
+
+def check_close(dev, ref, dtype):
+    atol, rtol = TOL[dtype]
+    err = np.abs(dev.float().cpu().numpy() - ref)
+    bad = err > atol + rtol * np.abs(ref)
+    assert not bad.any(), f"max err {err.max():.4g}, {bad.sum()} elements out of tolerance"
+
+
+def golden_for(cs):
+    """The reference record for this chain's tile grids (order-free key, see
+    make_bench_golden.key)."""
+    sc = cs.scenario()
+    stages = [[[s.grid.x, s.grid.y, s.grid.z], s.k_steps] for s in sc.stages]
+    deps = [[d.producer, d.consumer, [KINDS[type(d.policy)],
+                                      getattr(d.policy, "stride", getattr(d.policy, "kk", 0))]]
+            for d in sc.deps]
+    k = json.dumps(stages + deps)
+    assert k in GOLD, f"no reference fixture for {k} (rerun make_bench_golden.py)"
+    return GOLD[k]
+
+
+def check_sync(cs):
+    gold = golden_for(cs)
+    assert not cs.watchdog_fired()
+    assert {k: list(v) for k, v in cs.final_semaphores().items()} == gold["final_semaphores"]
+
+
+@functools.lru_cache(maxsize=2)
+def mlp_inputs(b):
+    g = torch.Generator().manual_seed(100 + b)
+    x = torch.randn(b, H, generator=g).half()
+    w1 = (torch.randn(FFN, H, generator=g) / H ** 0.5).half()
+    w2 = (torch.randn(H, FFN, generator=g) / FFN ** 0.5).half()
+    _, y_ref = O.mlp_chain(x.float().numpy(), w1.float().numpy(), w2.float().numpy(), "fp16")
+    return x.cuda(), w1.cuda(), w2.cuda(), y_ref
+
+
+def run_mlp(b, kw):
+    x, w1, w2, y_ref = mlp_inputs(b)
+    ch = ts.MlpChain(x, w1, w2, **{**kw, "keep_sems": True})
+    y = ch()
+    torch.cuda.synchronize()
+    check_sync(ch.cs)
+    check_close(y, y_ref, torch.float16)
+    # the benchmark relaunches the same chain: semaphores restored, result unchanged
+    ch.cs.keep_sems = False
+    ch.cs._desc = None
+    ch.cs.reset_semaphores()
+    y2 = ch().clone()
+    ch()
+    torch.cuda.synchronize()
+    assert torch.equal(y2, ch.y)
+    assert all(int(v) == 0 for d in ch.cs.deps for v in d.sem.cpu())
+
+
+HEADLINE = dict(policy=ts.RowSync(), tile_n=256, cta_group=2, prod_tile_n=512, cons_tile_n=512,
+                cons_order=ts.BandedColumnMajor(4))
+FIXED = [
+    # B=1024/2048 headline plans: 256x512 CTA-pair tiles, banded consumer, GeMM2 tail
+    (1024, dict(HEADLINE, cons_tail=(22, 2))),
+    (1024, dict(HEADLINE, cons_tail=(22, 3))),
+    (1024, dict(HEADLINE, prod_splits=2)),
+    (1024, dict(HEADLINE, policy=ts.TileSync(), prod_splits=3)),
+    (2048, dict(HEADLINE)),
+    (2048, dict(HEADLINE, policy=ts.TileSync(), cons_order=ts.RowMajor())),
+    # mid / small batch: split-K slices on 256x512 pairs and on single-CTA tiles
+    (256, dict(HEADLINE, prod_splits=4, cons_splits=2, cons_order=ts.RowMajor())),
+    (256, dict(HEADLINE, policy=ts.TileSync(), prod_splits=6, cons_splits=3,
+               cons_order=ts.RowMajor())),
+    (64, dict(policy=ts.RowSync(), tile_n=128, cta_group=1, prod_splits=3, cons_splits=1)),
+    (64, dict(policy=ts.TileSync(), tile_n=64, cta_group=1, swap_ab=True, prod_splits=3,
+              cons_splits=3)),
+    (1, dict(policy=ts.RowSync(), tile_n=256, cta_group=1, prod_splits=6, cons_splits=3)),
+    (1, dict(policy=ts.TileSync(), tile_n=256, cta_group=1, prod_splits=4, cons_splits=2)),
+    (1, dict(policy=ts.RowSync(), tile_n=32, cta_group=1, swap_ab=True, prod_splits=3,
+             cons_splits=3)),
+]
+
+
+@pytest.mark.parametrize("b,kw", FIXED, ids=[f"B{b}-{i}" for i, (b, _) in enumerate(FIXED)])
+def test_gpt3_mlp_fixed_plans(b, kw):
+    run_mlp(b, dict(kw, mode="fused"))
+
+
+@pytest.mark.parametrize("b", [1, 64, 256, 1024, 2048])
+def test_gpt3_mlp_planner_pick(b):
+    """Whatever the planner picks on this device (what bench.py runs), fused and stream."""
+    x, w1, w2, _ = mlp_inputs(b)
+    for mode in ("fused", "stream"):
+        kw, _ = planner.pick_mlp(x, w1, w2, mode=mode)
+        run_mlp(b, kw)
+
+
+@pytest.mark.parametrize("s,cg,z,ow,pol", [
+    (512, 2, 1, 512, ts.TileSync()), (512, 2, 2, 0, ts.RowSync()),
+    (512, 1, 4, 0, ts.TileSync()), (1024, 2, 1, 512, ts.RowSync())])
+def test_gpt3_attention_12_heads(s, cg, z, ow, pol):
+    """GPT-3 attention block, TP=8 shard: 12 heads of 128 over H=12288."""
+    g = torch.Generator().manual_seed(s)
+    heads = 12
+    x = torch.randn(s, H, generator=g).half()
+    wqkv = (torch.randn(3 * heads * 128, H, generator=g) / H ** 0.5).half()
+    w2 = (torch.randn(H, heads * 128, generator=g) / (heads * 128) ** 0.5).half()
+    ch = ts.AttentionChain(x.cuda(), wqkv.cuda(), w2.cuda(), second_policy=pol, cta_group=cg,
+                           keep_sems=True, qkv_splits=z, out_tile_n=ow)
+    ch()
+    torch.cuda.synchronize()
+    check_sync(ch.cs)
+    _, dot_ref, y_ref = O.attention_chain(x.float().numpy(), wqkv.float().numpy(),
+                                          w2.float().numpy(), "fp16")
+    check_close(ch.dot, dot_ref, torch.float16)
+    check_close(ch.y, y_ref, torch.float16)
+
+
+@pytest.mark.parametrize("tp,b,pw,cw,pol", [(8, 2048, 256, 0, ts.RowSync()),
+                                            (8, 2048, 512, 512, ts.TileSync()),
+                                            (1, 1024, 512, 512, ts.RowSync())])
+def test_llama_swiglu_tp_shard_bf16(tp, b, pw, cw, pol):
+    """LLaMA-8B SwiGLU MLP (H=4096, F=14336), the per-rank chain of a TP=tp shard, bf16."""
+    g = torch.Generator().manual_seed(tp * b)
+    hd, f = 4096, 14336 // tp
+    x = torch.randn(b, hd, generator=g).bfloat16()
+    wg = (torch.randn(f, hd, generator=g) / hd ** 0.5).bfloat16()
+    wu = (torch.randn(f, hd, generator=g) / hd ** 0.5).bfloat16()
+    wd = (torch.randn(hd, f, generator=g) / f ** 0.5).bfloat16()
+    wgu = ts.interleave_gate_up(wg, wu, pw)
+    ch = ts.SwigluChain(x.cuda(), wgu.cuda(), wd.cuda(), policy=pol, tile_n=256, cta_group=2,
+                        prod_tile_n=pw if pw == 512 else 0, cons_tile_n=cw, keep_sems=True)
+    ch()
+    torch.cuda.synchronize()
+    check_sync(ch.cs)
+    _, y_ref = O.swiglu_chain(x.float().numpy(), wg.float().numpy(), wu.float().numpy(),
+                              wd.float().numpy(), "bf16")
+    check_close(ch.y, y_ref, torch.bfloat16)
+
+
+@pytest.mark.parametrize("hw,c", planner.RESNET38_LAYERS)
+def test_resnet38_conv_pair_b32(hw, c):
+    """ResNet-38 3x3 conv pair at batch 32, Conv2DTileSync(9), every
+    configuration the conv sweep times for this layer."""
+    g = torch.Generator().manual_seed(hw)
+    b = 32
+    x = torch.randn(b, hw, hw, c, generator=g).half()
+    w1 = (torch.randn(c, 3, 3, c, generator=g) / (9 * c) ** 0.5).half()
+    w2 = (torch.randn(c, 3, 3, c, generator=g) / (9 * c) ** 0.5).half()
+    _, y_ref = O.conv_chain(x.float().numpy(), w1.float().numpy(), w2.float().numpy(), "fp16")
+    xd, w1d, w2d = x.cuda(), w1.cuda(), w2.cuda()
+    for kw in planner.conv_candidates(c, "fused", b * hw * hw):
+        ch = ts.ConvChain(xd, w1d, w2d, keep_sems=True, **kw)
+        ch()
+        torch.cuda.synchronize()
+        check_sync(ch.cs)
+        check_close(ch.y, y_ref, torch.float16)

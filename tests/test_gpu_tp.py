@@ -56,6 +56,23 @@ def run_group(x, w1, w2, world, mode="fused", **kw):
     return members, parts
 
 
+def check_counters(m, launches):
+    """Chain semaphores are back at zero; the all-reduce group's semaphores and done
+    counter are monotone: after e launches every semaphore holds e x (its posts per
+    launch) and the done counter e x tiles x cta_group (epoch scheme, ts_peer_desc)."""
+    cs = m.chain.cs
+    assert cs.epoch == launches
+    ard = cs.allreduce_dep()
+    g = ard.producer.grid
+    assert int(cs.allreduce_done.item()) == launches * g.x * g.y * cs.cta_group
+    for d in cs.deps:
+        vals = d.sem.cpu().tolist()
+        if d is ard:
+            assert all(v == launches * g.z for v in vals), vals
+        else:
+            assert all(v == 0 for v in vals)
+
+
 @pytest.mark.parametrize("world,mode,kw", [
     (1, "fused", dict(tile_n=256, cta_group=2)),
     (2, "fused", dict(tile_n=256, cta_group=2)),
@@ -71,8 +88,7 @@ def test_fused_allreduce_matches_sum_of_partials(world, mode, kw):
     for m in members:
         assert not m.chain.cs.watchdog_fired()
         assert torch.equal(m.y, expect)
-        assert int(m.chain.cs.allreduce_done.item()) == 0
-        assert all(int(v) == 0 for d in m.chain.cs.deps for v in d.sem.cpu())
+        check_counters(m, launches=3)
     # the TP result against the oracle's unsharded MLP (partials rounded per rank)
     _, ref = O.mlp_chain(x.float().numpy(), w1.float().numpy(), w2.float().numpy(), "fp16")
     err = np.abs(members[0].y.float().cpu().numpy() - ref)
@@ -89,4 +105,4 @@ def test_fused_allreduce_bf16_ragged_rows():
     for m in members:
         assert not m.chain.cs.watchdog_fired()
         assert torch.equal(m.y, expect)
-        assert int(m.chain.cs.allreduce_done.item()) == 0
+        check_counters(m, launches=3)
