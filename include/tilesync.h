@@ -236,6 +236,13 @@ typedef struct {
   void* trace;   /* optional device ts_trace_rec[trace_cap]; NULL = no tracing */
   int trace_cap;
   const ts_peer_desc* peers; /* TS_STAGE_ALLREDUCE only (host pointer; copied at launch) */
+  int cluster_pairs; /* 0/1: one CTA pair (or CTA) per cluster. 2: clusters of two CTA pairs
+                        (cta_group 2, tile_n 256, every GeMM stage tile_n 512, no dot /
+                        conv / all-reduce stage): a 256 x 512 tile runs as two 256 x 256
+                        pair tiles that share the activation rows by TMA multicast (24 KB
+                        instead of 32 KB of operands per SM and K-block) and keep their
+                        accumulators double-buffered in TMEM. Grids, semaphores, posts and
+                        waits are those of the 256 x 512 tile. */
 } ts_chain_desc;
 
 #define TS_SCRATCH_INTS 16
@@ -281,6 +288,13 @@ int ts_wait_kernel_launch(const int* flags, int n, void* stream);
  * is complete and visible; ts_stream_wait blocks `stream` until *sem >= value. */
 int ts_stream_signal(int* sem, int value, void* stream);
 int ts_stream_wait(const int* sem, int value, void* stream);
+
+/* Work items the current device runs at once for a chain of this geometry: CTAs
+ * (cta_group 1), CTA pairs (2) or two-pair clusters (cluster_pairs 2), capped at the
+ * number of clusters that are co-resident on the device — the wave size the planner's
+ * quantization arithmetic uses (reference gpu.waves, GpuConfig(num_sms)). */
+int ts_chain_units(int tile_n, int cta_group, int cluster_pairs, int swap_ab, int dtype,
+                   int* out);
 
 /* SM count of the current device. */
 int ts_device_sm_count(int* out);

@@ -36,7 +36,7 @@ EXPORTS = (
     "ts_abi_version", "ts_last_error", "ts_sem_count", "ts_post_target",
     "ts_consumer_wait", "ts_wait_steps", "ts_order_tile", "ts_avoid_wait_kernel",
     "ts_chain_launch", "ts_chain_grid", "ts_wait_kernel_launch",
-    "ts_device_sm_count", "ts_stream_signal", "ts_stream_wait",
+    "ts_device_sm_count", "ts_stream_signal", "ts_stream_wait", "ts_chain_units",
 )
 
 
@@ -79,7 +79,7 @@ class ChainDesc(ctypes.Structure):
         ("swap_ab", ctypes.c_int), ("flags", ctypes.c_int),
         ("num_ctas", ctypes.c_int), ("scratch", ctypes.c_void_p),
         ("trace", ctypes.c_void_p), ("trace_cap", ctypes.c_int),
-        ("peers", ctypes.POINTER(PeerDesc)),
+        ("peers", ctypes.POINTER(PeerDesc)), ("cluster_pairs", ctypes.c_int),
     ]
 
 
@@ -123,6 +123,7 @@ def load() -> ctypes.CDLL:
         "ts_chain_grid": ([ctypes.POINTER(ChainDesc), i, ip, ip], i),
         "ts_wait_kernel_launch": ([ctypes.c_void_p, i, ctypes.c_void_p], i),
         "ts_device_sm_count": ([ip], i),
+        "ts_chain_units": ([i, i, i, i, i, ip], i),
         "ts_stream_signal": ([ctypes.c_void_p, i, ctypes.c_void_p], i),
         "ts_stream_wait": ([ctypes.c_void_p, i, ctypes.c_void_p], i),
     }

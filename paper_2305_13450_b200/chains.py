@@ -30,7 +30,7 @@ class MlpChain:
                  cons_order: TileOrder = RowMajor(), swap_ab: bool = False,
                  prod_splits: int = 1, cons_splits: int = 1, prod_tile_n: int = 0,
                  cons_tile_n: int = 0, row_interleave: bool = False,
-                 cons_tail: tuple = (0, 1)):
+                 cons_tail: tuple = (0, 1), cluster_pairs: int = 1):
         """``row_interleave`` claims GeMM1 row r, GeMM2 row r, GeMM1 row r+1, ... (fused
         RowSync/TileSync, RowMajor orders): for inputs that arrive row by row
         (``run_host``), a row's GeMM2 tiles are not queued behind later rows' GeMM1 tiles
@@ -41,7 +41,8 @@ class MlpChain:
         self.y = torch.empty(m, w2.shape[0], dtype=x.dtype, device=x.device)
         self.cs = CuSync(tile_n=tile_n, mode=mode, reorder=reorder, keep_sems=keep_sems,
                          num_ctas=num_ctas, extra_flags=extra_flags, cta_group=cta_group,
-                         swap_ab=swap_ab, row_interleave=row_interleave)
+                         swap_ab=swap_ab, row_interleave=row_interleave,
+                         cluster_pairs=cluster_pairs)
         self.prod = self.cs.stage(x, w1, self.h, epilogue="gelu", order=prod_order, id="gemm1",
                                   splits=prod_splits, tile_n=prod_tile_n)
         self.cons = self.cs.stage(self.h, w2, self.y, order=cons_order, id="gemm2",
@@ -122,15 +123,18 @@ class SwigluChain:
     def __init__(self, x: torch.Tensor, w_gate_up: torch.Tensor, w_down: torch.Tensor,
                  policy: SyncPolicy = RowSync(), mode: str = "fused", tile_n: int = 256,
                  reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0,
-                 cta_group: int = 2, prod_tile_n: int = 0, cons_tile_n: int = 0):
+                 cta_group: int = 2, prod_tile_n: int = 0, cons_tile_n: int = 0,
+                 cluster_pairs: int = 1):
         """``prod_tile_n`` = 512 packs gate/up per 512-row block
-        (``interleave_gate_up(wg, wu, 512)``)."""
+        (``interleave_gate_up(wg, wu, 512)``); with ``cluster_pairs=2`` each pair holds
+        256 accumulator columns, so gate/up are packed per 256 rows
+        (``interleave_gate_up(wg, wu, 256)``) and both stages use tile_n=512."""
         m = x.shape[0]
         f = w_gate_up.shape[0] // 2
         self.h = torch.empty(m, f, dtype=x.dtype, device=x.device)
         self.y = torch.empty(m, w_down.shape[0], dtype=x.dtype, device=x.device)
         self.cs = CuSync(tile_n=tile_n, mode=mode, reorder=reorder, keep_sems=keep_sems,
-                         num_ctas=num_ctas, cta_group=cta_group)
+                         num_ctas=num_ctas, cta_group=cta_group, cluster_pairs=cluster_pairs)
         self.prod = self.cs.stage(x, w_gate_up, self.h, epilogue="swiglu", id="gate_up",
                                   tile_n=prod_tile_n)
         self.cons = self.cs.stage(self.h, w_down, self.y, id="down", tile_n=cons_tile_n)

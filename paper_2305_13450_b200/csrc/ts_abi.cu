@@ -128,37 +128,76 @@ int sm_count() {
   return n;
 }
 
-// `units` = tiles in flight at once (CTAs for CG=1, CTA pairs for CG=2).
-template <int BN, int CG, typename T, bool SW = false>
-int launch_one(const ts::ChainParams& p, int units, cudaStream_t stream) {
-  using C = ts::Cfg<BN, CG, SW>;
-  // the dynamic shared-memory opt-in is a per-device function attribute: set it once for
-  // every device this instantiation launches on (the caller's current device)
+// Per-device launch preparation of one kernel instantiation, done once per device: the
+// dynamic shared-memory opt-in (a per-device function attribute) and the number of
+// clusters the device can hold at once (a GPC whose SM count is not a multiple of the
+// cluster size leaves SMs idle; 0 = unknown).
+template <int BN, int CG, typename T, bool SW, bool QD>
+int prepare(int* max_clusters) {
+  using C = ts::Cfg<BN, CG, SW, QD>;
+  constexpr int kCluster = CG * (QD ? 2 : 1);
   constexpr int kMaxDev = 64;
-  static std::atomic<int> attr_set[kMaxDev];
+  static std::atomic<int> done[kMaxDev];
+  static std::atomic<int> mcs[kMaxDev];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   if (dev < 0 || dev >= kMaxDev) return fail(TS_ERR_CUDA, "device ordinal %d unsupported", dev);
-  if (attr_set[dev].load(std::memory_order_acquire) == 0) {
-    e = cudaFuncSetAttribute(ts::chain_kernel<BN, CG, T, SW>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  if (done[dev].load(std::memory_order_acquire) == 0) {
+    auto kern = ts::chain_kernel<BN, CG, T, SW, QD>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    attr_set[dev].store(1, std::memory_order_release);
+    int mc = 0;
+    if (kCluster > 1) {
+      int sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(sms - sms % kCluster, 1, 1);
+      cfg.blockDim = dim3(C::kThreads, 1, 1);
+      cfg.dynamicSmemBytes = C::kSmemBytes;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = kCluster;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        mc = 0;
+      }
+    }
+    mcs[dev].store(mc, std::memory_order_relaxed);
+    done[dev].store(1, std::memory_order_release);
   }
+  *max_clusters = mcs[dev].load(std::memory_order_relaxed);
+  return TS_OK;
+}
+
+// `units` = work items in flight at once: CTAs (CG=1), CTA pairs (CG=2) or two-pair
+// clusters (QD), capped at the co-resident cluster count so every launched cluster runs
+// from the start of the persistent kernel.
+template <int BN, int CG, typename T, bool SW = false, bool QD = false>
+int launch_one(const ts::ChainParams& p, int units, cudaStream_t stream) {
+  using C = ts::Cfg<BN, CG, SW, QD>;
+  constexpr int kCluster = CG * (QD ? 2 : 1);
+  int mc = 0;
+  int r = prepare<BN, CG, T, SW, QD>(&mc);
+  if (r) return r;
+  if (mc > 0 && units > mc) units = mc;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(units * CG, 1, 1);
+  cfg.gridDim = dim3(units * kCluster, 1, 1);
   cfg.blockDim = dim3(C::kThreads, 1, 1);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = kCluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, ts::chain_kernel<BN, CG, T, SW>, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, ts::chain_kernel<BN, CG, T, SW, QD>, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "chain_kernel launch");
   return TS_OK;
@@ -186,7 +225,11 @@ int launch_swapped(int bn, const ts::ChainParams& p, int units, cudaStream_t s) 
 }
 
 int launch_dispatch(int bn, int cg, int swap, int dtype, const ts::ChainParams& p, int units,
-                    cudaStream_t s) {
+                    cudaStream_t s, int np = 1) {
+  if (np == 2) {  // validated: cta_group 2, tile_n 256, normal layout
+    return dtype == TS_DTYPE_BF16 ? launch_one<256, 2, __nv_bfloat16, false, true>(p, units, s)
+                                  : launch_one<256, 2, __half, false, true>(p, units, s);
+  }
   if (swap) {
     return dtype == TS_DTYPE_BF16 ? launch_swapped<__nv_bfloat16>(bn, p, units, s)
                                   : launch_swapped<__half>(bn, p, units, s);
@@ -201,6 +244,7 @@ int launch_dispatch(int bn, int cg, int swap, int dtype, const ts::ChainParams& 
 }
 
 int tile_n_of(const ts_chain_desc* d) { return d->tile_n == 0 ? 256 : d->tile_n; }
+int cluster_pairs_of(const ts_chain_desc* d) { return d->cluster_pairs == 0 ? 1 : d->cluster_pairs; }
 int cta_group_of(const ts_chain_desc* d) {
   if (d->swap_ab) return 1;
   return d->cta_group == 0 ? 2 : d->cta_group;
@@ -246,6 +290,10 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
   const int cg = cta_group_of(d);
   if (cg != 1 && cg != 2) return fail(TS_ERR_VALUE, "cta_group must be 1 or 2 (got %d)", d->cta_group);
   if (cg == 2 && bn == 64) return fail(TS_ERR_VALUE, "cta_group 2 needs tile_n >= 128");
+  const int np = cluster_pairs_of(d);
+  if (np != 1 && np != 2) return fail(TS_ERR_VALUE, "cluster_pairs must be 0, 1 or 2 (got %d)", d->cluster_pairs);
+  if (np == 2 && (cg != 2 || bn != 256 || swap))
+    return fail(TS_ERR_CONFIG, "two-pair clusters need cta_group 2 and tile_n 256 (normal layout)");
   // reference-grid tile: rows of activations x columns of output
   const int tile_m = swap ? bn : 128 * cg;
   const int tile_n = swap ? 128 : bn;
@@ -270,6 +318,8 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     if (st.dtype != TS_DTYPE_F16 && st.dtype != TS_DTYPE_BF16)
       return fail(TS_ERR_TYPE, "stage %d: unknown dtype %d", s, st.dtype);
     if (st.dtype != dtype) return fail(TS_ERR_CONFIG, "stage %d: all stages must share a dtype", s);
+    if (np == 2 && st.kind != TS_STAGE_GEMM)
+      return fail(TS_ERR_CONFIG, "stage %d: two-pair clusters run GeMM stages only", s);
     if (st.kind == TS_STAGE_ATTN_DOT) {
       if (swap) return fail(TS_ERR_CONFIG, "stage %d: the attention dot stage needs normal tiles", s);
       if (st.m < 1 || st.n < bn || st.n % bn)
@@ -392,6 +442,8 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
                   "cta_group 2 and chain tile_n 256)", s, st.tile_n, tile_n);
     const int half_n = stage_half_n(st, bn, cg, swap);
     const int stage_tile_n = swap ? tile_n : half_n << wide;
+    if (np == 2 && !(wide == 1 && half_n == 256))
+      return fail(TS_ERR_CONFIG, "stage %d: two-pair clusters need tile_n 512 stages", s);
     if (st.n % stage_tile_n != 0)
       return fail(TS_ERR_CONFIG, "stage %d: n=%d is not a multiple of the tile width %d", s, st.n,
                   stage_tile_n);
@@ -482,6 +534,10 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       if (r) return r;
       r = make_tmap(&sp.tmap_b, st.b, st.n, st.k, st.ldb, st.dtype, swap ? 128 : half_n / cg);
       if (r) return r;
+      if (np == 2) {  // 64-row activation boxes: each CTA multicasts half of its rows
+        r = make_tmap(&sp.tmap_a_half, st.a, st.m, st.k, st.lda, st.dtype, 64);
+        if (r) return r;
+      }
     }
   }
   p->total_items = items;
@@ -775,13 +831,14 @@ int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
   const int dtype = desc->stages[0].dtype;
   int ctas = desc->num_ctas > 0 ? desc->num_ctas : sm_count();
   if (ctas <= 0) return fail(TS_ERR_CUDA, "could not query the SM count");
-  ctas /= cg;  // tiles in flight: CTAs (cg = 1) or CTA pairs (cg = 2)
-  if (ctas < 1) return fail(TS_ERR_VALUE, "num_ctas too small for cta_group %d", cg);
+  const int np = cluster_pairs_of(desc);
+  ctas /= cg * np;  // items in flight: CTAs (cg = 1), CTA pairs (cg = 2) or 2-pair clusters
+  if (ctas < 1) return fail(TS_ERR_VALUE, "num_ctas too small for cta_group %d x %d", cg, np);
   if (desc->mode == TS_MODE_FUSED) {
     p.item_lo = 0;
     p.item_hi = p.total_items;
     int grid = ctas < p.total_items ? ctas : p.total_items;
-    return launch_dispatch(bn, cg, desc->swap_ab, dtype, p, grid, s);
+    return launch_dispatch(bn, cg, desc->swap_ab, dtype, p, grid, s, np);
   }
   // Stream mode: the same kernel, one launch per stage, no semaphores — the
   // stream-synchronized baseline (reference Mode.STREAM engine.py:40-42).
@@ -807,7 +864,7 @@ int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
     q.item_hi = q.st[i].item_end;
     const int n = q.item_hi - q.item_lo;
     if (n <= 0) continue;  // e.g. a rank that owns no all-reduce tile
-    r = launch_dispatch(bn, cg, desc->swap_ab, dtype, q, ctas < n ? ctas : n, s);
+    r = launch_dispatch(bn, cg, desc->swap_ab, dtype, q, ctas < n ? ctas : n, s, np);
     if (r) return r;
   }
   return TS_OK;
@@ -837,6 +894,33 @@ int ts_stream_wait(const int* sem, int value, void* stream) {
   CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(sem),
                   static_cast<cuuint32_t>(value), CU_STREAM_WAIT_VALUE_GEQ);
   return r == CUDA_SUCCESS ? TS_OK : fail(TS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+}
+
+int ts_chain_units(int tile_n, int cta_group, int cluster_pairs, int swap_ab, int dtype,
+                   int* out) {
+  int sms = sm_count();
+  if (sms <= 0) return fail(TS_ERR_CUDA, "could not query the SM count");
+  const int cg = swap_ab ? 1 : (cta_group == 0 ? 2 : cta_group);
+  const int np = cluster_pairs == 0 ? 1 : cluster_pairs;
+  const int bn = tile_n == 0 ? 256 : tile_n;
+  int mc = 0, r = TS_OK;
+  const bool bf = dtype == TS_DTYPE_BF16;
+  if (np == 2) {
+    if (cg != 2 || bn != 256 || swap_ab)
+      return fail(TS_ERR_CONFIG, "two-pair clusters need cta_group 2 and tile_n 256");
+    r = bf ? prepare<256, 2, __nv_bfloat16, false, true>(&mc) : prepare<256, 2, __half, false, true>(&mc);
+  } else if (cg == 2) {
+    if (bn == 128) r = bf ? prepare<128, 2, __nv_bfloat16, false, false>(&mc) : prepare<128, 2, __half, false, false>(&mc);
+    else if (bn == 256) r = bf ? prepare<256, 2, __nv_bfloat16, false, false>(&mc) : prepare<256, 2, __half, false, false>(&mc);
+    else return fail(TS_ERR_VALUE, "cta_group 2 needs tile_n 128 or 256 (got %d)", bn);
+  } else if (np != 1) {
+    return fail(TS_ERR_VALUE, "cluster_pairs must be 0, 1 or 2 (got %d)", cluster_pairs);
+  }
+  if (r) return r;
+  int units = sms / (cg * np);
+  if (mc > 0 && mc < units) units = mc;
+  *out = units;
+  return TS_OK;
 }
 
 int ts_device_sm_count(int* out) {

@@ -71,6 +71,7 @@ __device__ __forceinline__ int wrap_inc(int e, int n) { return e + 1 == n ? 0 : 
 struct StageParams {
   CUtensorMap tmap_a;  // activations [m, k] K-major, 128-B swizzle
   CUtensorMap tmap_b;  // weights [n, k] K-major, 128-B swizzle
+  CUtensorMap tmap_a_half;  // two-pair clusters: activations, 64-row boxes (multicast halves)
   void* c;
   int m, n, k, ldc;
   int grid_x, grid_y;
@@ -140,7 +141,7 @@ struct ChainParams {
 // CTA pair) and UMMA N = BN over weight rows. Swapped layout (SW, small batch): UMMA M
 // runs over 128 weight rows and UMMA N = BN over activation rows, so every in-flight
 // smem byte of the dominant operand is weight — the HBM-bound regime.
-template <int BN, int CG, bool SW = false>
+template <int BN, int CG, bool SW = false, bool QD = false>
 struct Cfg {
   // CTA-pair 256-wide tiles stage operands through a ring of 16-KB chunks (one 128-row
   // x 64-K box each) instead of fixed slots, so a stage can use double-width tiles
@@ -150,13 +151,16 @@ struct Cfg {
   // Epilogue warps: 4 (one per TMEM lane quarter), or 8 for chunked tiles (two column
   // groups per lane quarter: a 256 x 512 tile's accumulator is single-buffered, so its
   // drain is on the MMA warp's critical path).
-  static constexpr int kEpiGroups = kChunked ? 2 : 1;
+  // (QD: each pair's 256-column accumulator is double-buffered: 4 warps, 256 threads and
+  // no register cap from a 384-thread CTA)
+  static constexpr int kEpiGroups = (kChunked && !QD) ? 2 : 1;
   static constexpr int kEpiThreads = 128 * kEpiGroups;
   static constexpr int kThreads = 128 + kEpiThreads;
   static constexpr int kChunkBytes = 16384;
   // A boxes and B boxes live in separate chunk rings (A ring first in smem)
-  static constexpr int kAChunks = 4;
-  static constexpr int kBChunks = 8;
+  // (two-pair clusters, QD: one A and one B chunk per K-block -> balanced 6 + 6)
+  static constexpr int kAChunks = QD ? 6 : 4;
+  static constexpr int kBChunks = QD ? 6 : 8;
   static constexpr int kChunks = kAChunks + kBChunks;
   static constexpr int kTileM = SW ? BN : 128 * CG;  // activation rows of a tile
   static constexpr int kTileN = SW ? 128 : BN;       // output columns of a tile
@@ -575,10 +579,22 @@ __device__ __forceinline__ void allreduce_rows(const ChainParams& p, const Stage
   }
 }
 
-template <int BN, int CG, typename T, bool SW>
-__global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
+// QD: clusters of two CTA pairs (4 CTAs). A work item is a 256 x 512 tile (the reference
+// tile of a double-width stage); pair p of the cluster computes its output columns
+// [256 p, 256 p + 256) as a 256 x 256 cta_group::2 tile with its own double-buffered TMEM
+// accumulator. Both pairs read the same 256 activation rows: every CTA loads 64 of its
+// 128 rows and multicasts them to the same-half CTA of the other pair, so each SM pulls
+// 24 KB of operands per 64-deep K-block instead of 32 KB (L2 -> SM bandwidth is what
+// bounds unicast 256 x 256 tiles), while the epilogue of one tile overlaps the MMAs of the
+// next (a 256 x 512 tile on one pair fills all of TMEM). Ring entries are freed by both
+// pairs' MMA commits (empty barriers count 2); the cluster leader claims items, hands the
+// id to the other three CTAs and posts once all four have stored.
+template <int BN, int CG, typename T, bool SW, bool QD = false>
+__global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
     chain_kernel(const __grid_constant__ ChainParams p) {
-  using C = Cfg<BN, CG, SW>;
+  using C = Cfg<BN, CG, SW, QD>;
+  static_assert(!QD || (CG == 2 && BN == 256 && !SW), "two-pair clusters: 256-wide CTA pairs");
+  constexpr int NP = QD ? 2 : 1;  // CTA pairs per cluster
   constexpr int kEpiThreads = C::kEpiThreads;
   constexpr int kEpiWarps = kEpiThreads / 32;
   static_assert(!SW || CG == 1, "swapped tiles use single-CTA MMAs");
@@ -609,24 +625,31 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = CG == 2 ? ptx::cluster_rank() : 0;
-  const bool leader = rank == 0;
+  const uint32_t qrank = CG == 2 ? ptx::cluster_rank() : 0;  // rank in the cluster
+  // (compile-time 0 / identities without QD, so one-pair kernels keep their registers)
+  const uint32_t rank = QD ? (qrank & 1) : qrank;     // CTA within its pair (row half)
+  const uint32_t pair = QD ? (qrank >> 1) : 0;        // pair within the cluster (column half)
+  const uint32_t plead = QD ? (qrank & ~1u) : 0;      // this pair's leader
+  const bool leader = rank == 0;                      // pair leader: MMA issuer, TMEM owner
+  const bool uleader = QD ? qrank == 0 : leader;      // cluster leader: scheduler, posts
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kFullRing; ++i) ptx::mbar_init(&full[i], 1);
-    for (int i = 0; i < kCommitRing; ++i) ptx::mbar_init(&empty[i], 1);
+    for (int i = 0; i < kCommitRing; ++i) ptx::mbar_init(&empty[i], NP);  // every pair's commit
     for (int i = 0; i < R; ++i) owner[i] = -1;
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tmem_full[i], 1);
       ptx::mbar_init(&tmem_empty[i], CG * kEpiWarps);
     }
-    for (int i = 0; i < kPeerRing; ++i) ptx::mbar_init(&peer_done[i], 1);
+    for (int i = 0; i < kPeerRing; ++i)
+      ptx::mbar_init(&peer_done[i], NP * CG > 1 ? NP * CG - 1 : 1);  // the other CTAs' stores
     ptx::mbar_init(dot_msg, 1);
     ptx::mbar_init(dot_done, 1);
     for (int i = 0; i < kTileRing; ++i) {
       ptx::mbar_init(&ti_full[i], 1);
-      // leader MMA warp + every epilogue warp of the pair + the peer's producer lane
-      ptx::mbar_init(&ti_empty[i], 1 + CG * kEpiWarps + (CG - 1));
+      // every pair's MMA warp + every epilogue warp of the cluster + the other CTAs'
+      // producer lanes
+      ptx::mbar_init(&ti_empty[i], NP + NP * CG * kEpiWarps + (NP * CG - 1));
     }
     *dot_count = 0;
     ptx::fence_barrier_init();
@@ -711,19 +734,18 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       for (int it = 0;; ++it) {
         int g;
         const int slot = it % kTileRing;
-        if (leader) {
-          if constexpr (CG == 2) {
-            ptx::mbar_wait(&ti_empty[slot], ((it / kTileRing) & 1) ^ 1);  // no data: slot reuse
-          } else {
-            ptx::mbar_wait(&ti_empty[slot], ((it / kTileRing) & 1) ^ 1);
-          }
+        if (uleader) {
+          ptx::mbar_wait(&ti_empty[slot], ((it / kTileRing) & 1) ^ 1);  // no data: slot reuse
           g = p.item_lo + atomicAdd(&p.scratch[0], 1);
           if (g >= p.item_hi) g = -1;
           ti_item[slot] = g;
           ptx::mbar_arrive(&ti_full[slot]);
           if constexpr (CG == 2) {
-            ptx::st_cluster_u32(ptx::mapa(&ti_item[slot], 1), static_cast<uint32_t>(g));
-            ptx::mbar_arrive_remote(ptx::mapa(&ti_full[slot], 1));
+#pragma unroll
+            for (int r = 1; r < NP * CG; ++r) {
+              ptx::st_cluster_u32(ptx::mapa(&ti_item[slot], r), static_cast<uint32_t>(g));
+              ptx::mbar_arrive_remote(ptx::mapa(&ti_full[slot], r));
+            }
           }
         } else {
           ptx::mbar_wait_cluster(&ti_full[slot], (it / kTileRing) & 1);
@@ -733,7 +755,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         if (g < 0) break;
         const Tile t = decode(p, g);
         const StageParams& st = p.st[t.s];
-        if (leader)
+        if (uleader)
           trace_event(p, ptx::global_timer(), 0, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
         if (st.kind == kStageDot || st.kind == kStageAllReduce)
           continue;  // pointwise stages: the epilogue warps run them
@@ -741,9 +763,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         const int act_row = SW ? t.tx * BN : t.tx * C::kTileM + static_cast<int>(rank) * 128;
         // a double-width tile's second B box (output columns [BN, 2 BN) of the pair
         // tile) starts BN weight rows further; each CTA holds its 128-row half of both
-        const int wide = C::kChunked ? st.wide : 0;
+        // QD: a double-width tile runs as one 256-wide MMA tile per pair (no second B box)
+        const int wide = (C::kChunked && !QD) ? st.wide : 0;
         const int hn = C::kChunked ? st.half_n : BN;  // columns per MMA
-        const int w_row = SW ? t.ty * 128 : t.ty * (hn << wide) + static_cast<int>(rank) * (hn / CG);
+        const int w_row = SW ? t.ty * 128
+                             : t.ty * (hn << (QD ? 1 : wide)) + static_cast<int>(pair) * hn +
+                                   static_cast<int>(rank) * (hn / CG);
         const int d = st.in_dep;
         const int bh = b_hint ? b_hint : (st.grid_x == 1 ? 1 : 2);
         const uint64_t pol_b = bh == 1 ? pol_first : (bh == 2 ? pol_normal : pol_last);
@@ -760,7 +785,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           const Grid3 pg{dp.pgx, dp.pgy, dp.pgz};
           Wait w = consumer_wait(dp.policy, dp.param, t.tx, t.ty, ks, pg, dp.pgz);
           if (w.sem < 0) return;
-          if (leader)
+          if (uleader)
             trace_event(p, ptx::global_timer(), 1, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
                         t.ty, t.tz);
           // Halo (extension): a 3x3 window of output rows [m0, m0 + tile_m) reads input
@@ -785,7 +810,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           else if (!((done_mask >> d) & 1) &&
                    sem_wait_dep(p, d, dp.sem + w.sem, w.expected, h1, e1, h2, e2, h3, e3, h4, e4))
             done_mask |= 1u << d;
-          if (leader)
+          if (uleader)
             trace_event(p, ptx::global_timer(), 2, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
                         t.ty, t.tz);
           ptx::fence_proxy_async_global();
@@ -847,7 +872,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         // the activation (A) box of K-block kb into `dst`, completing on barrier fb; conv:
         // cc = conv_coords(kb)
         auto load_a = [&](uint8_t* dst, uint64_t* fb, int kb, int cc) {
-          const uint32_t fbc = CG == 2 ? ptx::mapa(fb, 0) : 0;
+          const uint32_t fbc = CG == 2 ? ptx::mapa(fb, plead) : 0;
           if (conv) {
             // im2col box: 128 consecutive output pixels' inputs at filter tap (r, s), 64
             // channels from c0; the map's bounding box starts at (-1, -1), so pixel
@@ -860,6 +885,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             } else {
               ptx::tma_load_im2col(dst, &st.tmap_a, fb, c0, cq - 1, cp - 1, cn, s, r, pol_a);
             }
+          } else if constexpr (QD) {
+            // this CTA's 64 of its half's 128 rows, to the same half of both pairs
+            const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (2 + rank)));
+            ptx::tma_load_2d_pair_mc(dst + pair * (C::kChunkBytes / 2), &st.tmap_a_half, fbc,
+                                     kb * kBK, act_row + static_cast<int>(pair) * 64, mask, pol_a);
           } else if constexpr (CG == 2) {
             ptx::tma_load_2d_pair(dst, &st.tmap_a, fbc, kb * kBK, act_row, pol_a);
           } else {
@@ -904,7 +934,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             }
           }
           uint64_t* fb = &full[kq % kFullRing];
-          const uint32_t fbc = CG == 2 ? ptx::mapa(fb, 0) : 0;  // the leader CTA's barrier
+          const uint32_t fbc = CG == 2 ? ptx::mapa(fb, plead) : 0;  // the pair leader's barrier
           if (leader) {
             const int nc = 2 + wide;
             // chunked: A box (128 rows) + 1-2 B boxes of hn / 2 rows, 128 B each
@@ -992,13 +1022,13 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       uint32_t u = 0;  // TMEM accumulator-slot uses (a double-width tile takes two)
 #pragma unroll 1
       for (int it = 0;; ++it) {
-        const int g = ring_take(it, false);
+        const int g = ring_take(it, QD && !uleader);
         if (g < 0) break;
         const StageParams& sp = p.st[stage_of(p, g)];
         if (sp.kind == kStageDot || sp.kind == kStageAllReduce)
           continue;  // no MMA, no accumulator buffer
         const int kblocks = sp.k_blocks / item_slices(sp, g - sp.item_begin);
-        const int wide = C::kChunked ? sp.wide : 0;
+        const int wide = (C::kChunked && !QD) ? sp.wide : 0;
         // instruction descriptor: N = the stage's columns per MMA (chunked stages)
         const uint32_t idesc = C::kChunked ? ptx::idesc_f16(128 * CG, sp.half_n, AbFormat<T>::value)
                                            : kIdesc;
@@ -1066,7 +1096,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             }
             // one commit frees every ring entry of the group's K-blocks
             if (gi + 1 == group || kb + 1 == kblocks) {
-              if constexpr (CG == 2) {
+              if constexpr (QD) {
+                ptx::umma_commit_pair_mask(&empty[cid % kCommitRing], 0xF);  // all 4 CTAs' rings
+              } else if constexpr (CG == 2) {
                 ptx::umma_commit_pair(&empty[cid % kCommitRing]);
               } else {
                 ptx::umma_commit(&empty[cid % kCommitRing]);
@@ -1086,7 +1118,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         }
         if (lane == 0) {
           for (int j = 0; j <= wide; ++j) {
-            if constexpr (CG == 2) {
+            if constexpr (QD) {
+              ptx::umma_commit_pair_mask(&tmem_full[(u + j) & 1],
+                                         static_cast<uint16_t>(3u << plead));  // this pair
+            } else if constexpr (CG == 2) {
               ptx::umma_commit_pair(&tmem_full[(u + j) & 1]);
             } else {
               ptx::umma_commit(&tmem_full[(u + j) & 1]);
@@ -1137,7 +1172,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
     uint32_t tmem_empty_remote[2] = {0, 0};
     if constexpr (CG == 2) {
       if (!leader) {
-        for (int i = 0; i < 2; ++i) tmem_empty_remote[i] = ptx::mapa(&tmem_empty[i], 0);
+        for (int i = 0; i < 2; ++i) tmem_empty_remote[i] = ptx::mapa(&tmem_empty[i], plead);
       }
     }
     // Compute dot tile (tx, ty) of stage ds with the 128 epilogue threads (its wait is
@@ -1189,7 +1224,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
     uint32_t dmsg = 0, ddone = 0;  // dot_msg / dot_done phases (peer / leader)
 #pragma unroll 1
     for (int it = 0;; ++it) {
-      const int g = ring_take(it, CG == 2 && !leader);
+      const int g = ring_take(it, CG == 2 && !uleader);
       if (g < 0) break;
       const Tile t = decode(p, g);
       const StageParams& st = p.st[t.s];
@@ -1243,12 +1278,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         run_dot(t.s, t.tx, t.ty, t.tb);
         continue;
       }
-      const int wide = C::kChunked ? st.wide : 0;
+      const int wide = (C::kChunked && !QD) ? st.wide : 0;
       const int hn = C::kChunked ? st.half_n : BN;  // accumulator columns per slot
       for (int j = 0; j <= wide; ++j)  // arrived by the MMA commits
         ptx::mbar_wait(&tmem_full[(u + j) & 1], ((u + j) >> 1) & 1);
       ptx::tc_fence_after();
-      if (threadIdx.x == 128 && leader && p.trace != nullptr)  // epilogue begin (extension)
+      if (threadIdx.x == 128 && uleader && p.trace != nullptr)  // epilogue begin (extension)
         trace_event(p, ptx::global_timer(), 7, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
       const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
       const uint32_t t_lane = lane_base + (u & 1) * C::kAccCols;
@@ -1365,7 +1400,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
       const int row = t.tx * C::kTileM + static_cast<int>(rank) * 128 + ew * 32 + lane;
       const bool row_ok = row < st.m;
       T* crow = reinterpret_cast<T*>(st.c) + static_cast<size_t>(row) * st.ldc;
-      const int acc_cols = hn << wide;  // accumulator columns of this tile
+      const int acc_cols = hn << wide;  // accumulator columns of this tile (this pair's)
+      // first output column of this pair's accumulator (QD: the pair's half of the unit)
+      const int col0 = QD ? (2 * t.ty + static_cast<int>(pair)) * acc_cols : t.ty * acc_cols;
       // full-sector (32-B) stores when the output rows are 32-B aligned
       const bool v8ok = ((reinterpret_cast<uintptr_t>(st.c) | (st.ldc * sizeof(T))) & 31) == 0;
       constexpr int G = C::kEpiGroups;
@@ -1380,7 +1417,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         // partial plane of one CTA: [acc_cols / 32 chunks][128 rows][32 floats], so a
         // warp's 32 rows of one chunk are 4 KB contiguous (coalesced writes and reads)
         const size_t plane = static_cast<size_t>(128) * acc_cols;
-        float* mine = st.ws + (static_cast<size_t>(tile_id * t.z + t.tz) * CG + rank) * plane;
+        float* mine = st.ws + (static_cast<size_t>(tile_id * t.z + t.tz) * (CG * NP) + qrank) * plane;
         const int span = acc_cols / G;
         // only rows < m carry data (small batch: a 128-row tile may hold a single row)
         const int row0 = t.tx * C::kTileM + static_cast<int>(rank) * 128;
@@ -1410,10 +1447,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         }
         __threadfence();
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-        if (threadIdx.x == 128 && leader && p.trace != nullptr)  // partials written (ext.)
+        if (threadIdx.x == 128 && uleader && p.trace != nullptr)  // partials written (ext.)
           trace_event(p, ptx::global_timer(), 9, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
         if (threadIdx.x == 128) {
-          const int half_id = tile_id * CG + static_cast<int>(rank);
+          const int half_id = tile_id * CG * NP + static_cast<int>(qrank);
           const int old = atomicAdd(&st.cnt[half_id], 1);
           *split_flag = (old == t.z - 1);
           if (old == t.z - 1) st.cnt[half_id] = 0;  // restore the zero invariant
@@ -1423,8 +1460,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
           ptx::fence_acq_rel_gpu();
           // Reduction, warp-cooperative: one step = 4 rows x 32 columns of one chunk
           // (512 B per slice, lane l: row r0 + l / 8, columns (l % 8) * 4 .. + 4).
-          const float* base = st.ws + static_cast<size_t>(tile_id) * t.z * CG * plane +
-                              static_cast<size_t>(rank) * plane;
+          const float* base = st.ws + static_cast<size_t>(tile_id) * t.z * (CG * NP) * plane +
+                              static_cast<size_t>(qrank) * plane;
           const bool gl = st.epilogue == TS_EPI_GELU;
           const bool rl = st.epilogue == TS_EPI_RELU;
           const int nr4 = (valid + 3) / 4;          // 4-row groups holding data
@@ -1437,11 +1474,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
             const int grow = row0 + r0 + (lane >> 3);
             if (grow < st.m) {
               T* dst = reinterpret_cast<T*>(st.c) + static_cast<size_t>(grow) * st.ldc +
-                       t.ty * acc_cols + chunk * 32 + (lane & 7) * 4;
+                       col0 + chunk * 32 + (lane & 7) * 4;
               *reinterpret_cast<uint2*>(dst) = make_uint2(pack2<T>(o[0], o[1]), pack2<T>(o[2], o[3]));
             }
           };
-          const size_t zs = static_cast<size_t>(CG) * plane;
+          const size_t zs = static_cast<size_t>(CG * NP) * plane;
           const int ss = kEpiWarps;
           const uint64_t pol_ef =
               (p.flags >> 26) & 1 ? ptx::policy_evict_normal() : ptx::policy_evict_first();
@@ -1479,7 +1516,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
 #pragma unroll
                 for (int zz = 0; zz < 4; ++zz)
                   v[j][zz] = (sidx < steps && z0 + zz < t.z)
-                                 ? __ldcg(reinterpret_cast<const float4*>(base + (z0 + zz) * CG * plane + off))
+                                 ? __ldcg(reinterpret_cast<const float4*>(base + (z0 + zz) * zs + off))
                                  : make_float4(0.f, 0.f, 0.f, 0.f);
               }
 #pragma unroll
@@ -1507,7 +1544,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         // column group stores its 1/G of the output columns
         const int half = acc_cols / 2;
         const int span = half / G;
-        T* out = crow + t.ty * half + eg * span;
+        T* out = crow + (QD ? (2 * t.ty + static_cast<int>(pair)) * half : t.ty * half) + eg * span;
 #pragma unroll 1
         for (int cc = 0; cc < span / 32; ++cc) {
           const int x = eg * span + cc * 32;
@@ -1526,7 +1563,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         }
         release_tmem();
       } else {
-        T* out = crow + t.ty * acc_cols;
+        T* out = crow + col0;
         const bool gl = st.epilogue == TS_EPI_GELU;
         const bool rl = st.epilogue == TS_EPI_RELU;
         // Column group eg stores accumulator columns [eg * span, (eg + 1) * span); slot
@@ -1560,13 +1597,13 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW>::kThreads, 1)
         }
       }
       }  // normal layout
-      if (threadIdx.x == 128 && leader && p.trace != nullptr)  // epilogue stores issued
+      if (threadIdx.x == 128 && uleader && p.trace != nullptr)  // epilogue stores issued
         trace_event(p, ptx::global_timer(), 8, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
       // stage.post(): every epilogue thread's stores (of both CTAs of a pair)
       // happen-before the release below.
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
       if (threadIdx.x == 128) {
-        if (CG == 2 && !leader) {
+        if (CG == 2 && !uleader) {
           __threadfence();
           ptx::mbar_arrive_remote(ptx::mapa(&peer_done[local % kPeerRing], 0));
         } else {

@@ -160,6 +160,21 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       : "memory");
 }
 
+// CTA-pair multicast variant: the box lands at the same CTA-relative offset in every CTA
+// of `mask`; each destination's bytes are counted on its own pair leader's barrier
+// (`bar_cluster` = this CTA's pair-leader barrier: .cta_group::2 resolves the leader per
+// destination pair, as CUTLASS's SM100_TMA_2SM_LOAD_MULTICAST does).
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* m,
+                                                    uint32_t bar_cluster, int c0, int c1,
+                                                    uint16_t mask, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "h"(mask), "r"(c0), "r"(c1),
+      "l"(cache_hint)
+      : "memory");
+}
+
 // 4-D im2col load (NHWC): `pixelsPerColumn` consecutive pixels of the map's bounding box
 // from (w, h, n), channels [c, c + channelsPerPixel), each pixel shifted by the filter
 // tap offsets (ow, oh); out-of-image pixels read as zero.
@@ -371,6 +386,16 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], %1;" ::"r"(smem_u32(bar)),
       "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+// Pair commit to the barrier at the same offset in every CTA of `mask` (two pairs sharing
+// multicast operands: the ring entries of all four CTAs).
+__device__ __forceinline__ void umma_commit_pair_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
       : "memory");
 }
 

@@ -132,6 +132,10 @@ class CuSync:
     extra_flags: int = 0
     swap_ab: bool = False
     row_interleave: bool = False  # claim tiles row by row across two GeMM stages
+    # 2: clusters of two CTA pairs sharing the activation rows by TMA multicast; a tile
+    # (256 x 512, every GeMM stage tile_n=512) runs as two 256 x 256 pair tiles with
+    # double-buffered accumulators (ts_chain_desc.cluster_pairs)
+    cluster_pairs: int = 1
     device: torch.device | None = None
     stages: list[CuStage] = field(default_factory=list)
     deps: list[CuDep] = field(default_factory=list)
@@ -147,6 +151,9 @@ class CuSync:
             raise ConfigError(f"tile_n must be 64, 128 or 256, got {self.tile_n}")
         if self.cta_group not in (1, 2) or (self.cta_group == 2 and self.tile_n == 64):
             raise ConfigError("cta_group must be 1 or 2 (2 needs tile_n >= 128)")
+        if self.cluster_pairs not in (1, 2) or (self.cluster_pairs == 2 and (
+                self.cta_group != 2 or self.tile_n != 256 or self.swap_ab)):
+            raise ConfigError("cluster_pairs=2 needs cta_group=2, tile_n=256 (normal layout)")
         self._desc: _lib.ChainDesc | None = None
         self._peers: _lib.PeerDesc | None = None
         self._ar_done: torch.Tensor | None = None
@@ -160,13 +167,21 @@ class CuSync:
         swapped."""
         return self.tile_n if self.swap_ab else BM * self.cta_group
 
-    def _check_open(self) -> None:
+    def _check_open(self, kind: str = "gemm") -> None:
         """Stages may not follow an all-reduce stage: it stages peer vectors in the
-        operand ring, which is idle only when no GeMM item comes after it."""
+        operand ring, which is idle only when no GeMM item comes after it. Two-pair
+        clusters run GeMM stages only."""
+        if kind != "gemm" and self.cluster_pairs == 2:
+            raise ConfigError(f"cluster_pairs=2 runs GeMM stages only (not {kind})")
         if len(self.stages) >= _lib.TS_MAX_STAGES:
             raise ConfigError(f"at most {_lib.TS_MAX_STAGES} stages per chain")
         if any(st.kind == "allreduce" for st in self.stages):
             raise ConfigError("the all-reduce stage must be the chain's last stage")
+
+    @property
+    def ctas_per_tile(self) -> int:
+        """CTAs that compute one tile: 1, 2 (a CTA pair) or 4 (two pairs)."""
+        return self.cta_group * self.cluster_pairs
 
     def _check_tile_n(self, tile_n: int) -> None:
         """Per-stage tile width: 0 (the chain's), or 384 / 512 (two MMAs of 192 / 256
@@ -187,6 +202,8 @@ class CuSync:
         chains with ``cta_group=2, tile_n=256`` only)."""
         self._check_tile_n(tile_n)
         self._check_open()
+        if self.cluster_pairs == 2 and tile_n != 512:
+            raise ConfigError("cluster_pairs=2 runs tile_n=512 (256 x 512) GeMM stages")
         if epilogue not in _EPI:
             raise ConfigError(f"unknown epilogue {epilogue!r}")
         for t, name in ((a, "a"), (b, "b"), (c, "c")):
@@ -211,13 +228,13 @@ class CuSync:
             tiles = st.grid.x * st.grid.y
             st.ws = torch.empty(tiles * tail[1] * self.tile_m * st.width, dtype=torch.float32,
                                 device=a.device)
-            st.cnt = torch.zeros(tiles * self.cta_group, dtype=torch.int32, device=a.device)
+            st.cnt = torch.zeros(tiles * self.ctas_per_tile, dtype=torch.int32, device=a.device)
         if splits > 1:
             # fp32 partials [tile][slice][tile_m rows][width] and per-(tile, CTA) counters
             tiles = st.grid.x * st.grid.y
             st.ws = torch.empty(tiles * splits * self.tile_m * st.width, dtype=torch.float32,
                                 device=a.device)
-            st.cnt = torch.zeros(tiles * self.cta_group, dtype=torch.int32, device=a.device)
+            st.cnt = torch.zeros(tiles * self.ctas_per_tile, dtype=torch.int32, device=a.device)
         self.stages.append(st)
         self.device = a.device
         self._desc = None
@@ -229,7 +246,7 @@ class CuSync:
         Dropout(Softmax(XQ . XV)) . XK per 128-column head, with ``qkv`` [m, 3n] holding
         [Q heads | K heads | V heads]. Column-tile local, as its StridedSync dependency
         defines it; dropout p = 0 (inference)."""
-        self._check_open()
+        self._check_open("dot")
         for t, name in ((qkv, "qkv"), (out, "out")):
             if t.dim() != 2 or t.stride(1) != 1 or t.dtype not in _DT or not t.is_cuda:
                 raise ValueError(f"{name} must be a row-major fp16/bf16 CUDA matrix")
@@ -250,7 +267,7 @@ class CuSync:
         ``out`` NHWC [N, H, W, Cout]. Output rows are the N*H*W pixels, columns the output
         channels; the A operand is gathered by an im2col TMA map (zero padding at the
         image border). Feed it from another stage with ``Conv2DTileSync(9)``."""
-        self._check_open()
+        self._check_open("conv")
         if epilogue not in ("none", "relu", "gelu"):
             raise ConfigError(f"unsupported conv epilogue {epilogue!r}")
         if x.dim() != 4 or out.dim() != 4 or w.dim() != 4 or tuple(w.shape[1:3]) != (3, 3):
@@ -295,6 +312,7 @@ class CuSync:
             raise ConfigError("the all-reduce stage sums a normal-layout GeMM stage's output")
         if any(st.kind == "allreduce" for st in self.stages):
             raise ConfigError("a chain has at most one all-reduce stage")
+        self._check_open("allreduce")
         c = producer.c
         st = CuStage(self, len(self.stages), id or "allreduce", c, c, c, "none", RowMajor(),
                      kind="allreduce", tile_n=producer.tile_n)
@@ -421,6 +439,7 @@ class CuSync:
                    | (_lib.TS_FLAG_ROW_INTERLEAVE if self.row_interleave else 0)
                    | self.extra_flags)
         d.num_ctas = self.num_ctas
+        d.cluster_pairs = self.cluster_pairs
         if self._scratch is None:
             self._scratch = torch.zeros(_lib.TS_SCRATCH_INTS, dtype=torch.int32,
                                         device=self.device)

@@ -40,7 +40,22 @@ def _check_watchdog(ch, kw) -> None:
         raise RuntimeError(f"semaphore watchdog fired while timing candidate {kw}")
 
 
-def candidates(m: int, mode: str, n2: int | None = None, units: int = 74):
+def chain_units(tile_n: int = 256, cta_group: int = 2, cluster_pairs: int = 1,
+                swap_ab: bool = False, dtype: torch.dtype = torch.float16) -> int:
+    """Work items the current device runs at once for this chain geometry (CTAs, CTA
+    pairs or two-pair clusters; co-resident cluster count from the driver)."""
+    import ctypes
+
+    from . import _lib
+    out = ctypes.c_int(0)
+    _lib.check(_lib.load().ts_chain_units(tile_n, cta_group, cluster_pairs, int(swap_ab),
+                                          _lib.TS_DTYPE_BF16 if dtype == torch.bfloat16
+                                          else _lib.TS_DTYPE_F16, ctypes.byref(out)))
+    return out.value
+
+
+def candidates(m: int, mode: str, n2: int | None = None, units: int = 74,
+               qd_units: int | None = None):
     """Candidate chain configurations for `m` activation rows.
 
     Large batch: normal tiles (activations on the UMMA M side), CTA pairs or single CTAs,
@@ -93,6 +108,22 @@ def candidates(m: int, mode: str, n2: int | None = None, units: int = 74):
                         out.append(dict(policy=RowSync(), mode=mode, tile_n=tn, cta_group=cg,
                                         cons_order=co, prod_tile_n=512, cons_tile_n=512,
                                         prod_splits=z1, cons_tail=(rem, zt)))
+        if (cg, tn) == (2, 256) and m >= 256:
+            # two-pair clusters: the 256 x 512 tile on two CTA pairs sharing the activation
+            # rows by multicast (24 KB of operands per SM and K-block, double-buffered
+            # accumulators): half the tile time of one pair, so GeMM1 at B=1024 is 1.3
+            # waves of 37 clusters instead of 0.65 of 74 pairs
+            qd = dict(tile_n=tn, cta_group=cg, cluster_pairs=2, prod_tile_n=512,
+                      cons_tile_n=512)
+            qu = qd_units or max(1, units // 2)
+            for pol, co, z1 in itertools.product(pols, orders, (1, 2, 3)):
+                out.append(dict(qd, policy=pol, mode=mode, cons_order=co, prod_splits=z1))
+            if n2 and n2 % 512 == 0:
+                rem = (-(-m // 256) * (n2 // 512)) % qu
+                if rem:
+                    for co, z1, zt in itertools.product(orders, (1, 2, 3), (2, 3)):
+                        out.append(dict(qd, policy=RowSync(), mode=mode, cons_order=co,
+                                        prod_splits=z1, cons_tail=(rem, zt)))
     return out
 
 
@@ -111,6 +142,8 @@ def describe(kw) -> dict:
          "consumer_order": type(co).__name__ + (f"({co.band})" if hasattr(co, "band") else "")}
     if kw.get("cons_tail", (0, 1))[0]:
         d["consumer_tail"] = list(kw["cons_tail"])  # (tiles, split-K slices) of the last wave
+    if kw.get("cluster_pairs", 1) == 2:
+        d["cluster_pairs"] = 2  # the 256 x 512 tile on two multicast-sharing CTA pairs
     return d
 
 
@@ -124,8 +157,9 @@ def pick_mlp(x, w1, w2, mode="fused", tie=0.015):
     table = []
     best, best_us = None, float("inf")
     timed = []
-    sms = torch.cuda.get_device_properties(x.device).multi_processor_count
-    for kw in candidates(x.shape[0], mode, n2=w2.shape[0], units=sms // 2):
+    with torch.cuda.device(x.device):
+        units, qd_units = chain_units(), chain_units(cluster_pairs=2)
+    for kw in candidates(x.shape[0], mode, n2=w2.shape[0], units=units, qd_units=qd_units):
         ch = MlpChain(x, w1, w2, **kw)
         us = _time(ch)
         _check_watchdog(ch, kw)

@@ -79,7 +79,11 @@ def run_mlp(b, kw):
     ch = ts.MlpChain(x, w1, w2, **{**kw, "keep_sems": True})
     y = ch()
     torch.cuda.synchronize()
-    check_sync(ch.cs)
+    if kw.get("mode", "fused") == "fused":
+        check_sync(ch.cs)
+    else:  # the stream-synchronized baseline posts nothing
+        assert not ch.cs.watchdog_fired()
+        assert all(int(v) == 0 for d in ch.cs.deps for v in d.sem.cpu())
     check_close(y, y_ref, torch.float16)
     # the benchmark relaunches the same chain: semaphores restored, result unchanged
     ch.cs.keep_sems = False
@@ -102,6 +106,12 @@ FIXED = [
     (1024, dict(HEADLINE, policy=ts.TileSync(), prod_splits=3)),
     (2048, dict(HEADLINE)),
     (2048, dict(HEADLINE, policy=ts.TileSync(), cons_order=ts.RowMajor())),
+    # two-pair clusters (the 256x512 tile on two multicast-sharing CTA pairs)
+    (1024, dict(HEADLINE, cluster_pairs=2)),
+    (1024, dict(HEADLINE, cluster_pairs=2, cons_tail=(22, 3))),
+    (1024, dict(HEADLINE, cluster_pairs=2, policy=ts.TileSync(), prod_splits=2)),
+    (2048, dict(HEADLINE, cluster_pairs=2, cons_tail=(7, 2))),
+    (256, dict(HEADLINE, cluster_pairs=2, prod_splits=3, cons_order=ts.RowMajor())),
     # mid / small batch: split-K slices on 256x512 pairs and on single-CTA tiles
     (256, dict(HEADLINE, prod_splits=4, cons_splits=2, cons_order=ts.RowMajor())),
     (256, dict(HEADLINE, policy=ts.TileSync(), prod_splits=6, cons_splits=3,
