@@ -61,7 +61,7 @@ def summarize(cs, label):
             lead = [mb[k] - start[k].t_ns for k in keys]
             # ideal tensor cycles of one tile: 4096 MAC/clk per SM (8192 per CTA pair)
             macs = cs.tile_m * st.width * st.k // max(1, st.splits)
-            ideal = macs / (4096 * (2 if cs.cta_group == 2 else 1))
+            ideal = macs / (4096 * (2 if cs.cta_group == 2 else 1) * cs.cluster_pairs)
             eff = (f", {sum(cyc) / len(cyc):.0f} cycles = {ideal / (sum(cyc) / len(cyc)) * 100:.0f}%"
                    f" of the MMA floor") if cyc and st.kind == "gemm" else ""
             print(f"  {st.id}: MMA span mean {sum(mma) / len(mma) / 1e3:.1f} us{eff}, "
@@ -146,8 +146,9 @@ def main():
         z1, z2 = zs[0], (zs[1] if len(zs) > 1 else 1)
         widths = [int(w) for w in parts[7].split("/")] if len(parts) > 7 else [0, 0]
         tail = tuple(int(t) for t in parts[8].split(",")) if len(parts) > 8 else (0, 1)
+        qd = int(parts[9]) if len(parts) > 9 else 1
         policy = {"row": ts.RowSync(), "tile": ts.TileSync()}[pol]
-        kw = dict(prod_splits=z1, cons_splits=z2, cons_tail=tail)
+        kw = dict(prod_splits=z1, cons_splits=z2, cons_tail=tail, cluster_pairs=qd)
         kw.update(dict(swap_ab=True, tile_n=swap_tn) if swap_tn else
                   dict(prod_tile_n=widths[0], cons_tile_n=widths[1]))
         ch = ts.MlpChain(x, w1, w2, policy=policy, mode=mode, prod_order=order(po),
