@@ -140,8 +140,8 @@ typedef struct {
                         (tile_m = rows of a tile: 128 x cta_group, or tile_n swapped;
                         tile_cols = accumulator columns: the stage's tile width, or 128
                         swapped)                                                       */
-  int* counters;     /* splits > 1: device int32[tiles * cta_group], zero on entry
-                        (kept zero)                                                    */
+  int* counters;     /* splits > 1: device int32[2 * tiles * cta_group] (per tile half:
+                        slice arrivals, then partials ready), zero on entry (kept zero) */
   int kind;          /* ts_stage_kind */
   int conv_n, conv_h, conv_w; /* TS_STAGE_CONV2D: image batch, height, width (3x3 kernel,
                         stride 1, padding 1: output H x W = input H x W); m = n*h*w,

@@ -13,14 +13,13 @@
 #include <string>
 
 #include "tilesync.h"
-#include "ts_chain_kernel.cuh"
+#include "ts_launch.h"
 #include "ts_policy.cuh"
 
-namespace {
+namespace ts_host {
 
 thread_local std::string g_err;
 
-int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 int fail(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -34,6 +33,15 @@ int fail(int code, const char* fmt, ...) {
 int cuda_fail(cudaError_t e, const char* what) {
   return fail(TS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
+
+}  // namespace ts_host
+
+namespace {
+
+using ts_host::cuda_fail;
+using ts_host::fail;
+using ts_host::launch_one;
+using ts_host::prepare;
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -54,9 +62,52 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// Encoded tensor maps, keyed by everything that enters the encoding (pointer, shape,
+// stride, dtype, box, kind): ts_chain_launch re-derives every map of a chain on each call,
+// and cuTensorMapEncode* costs microseconds of host time per map against 30-70 us chains
+// ("may cache TMA descriptors keyed by (ptr, shape, stride)"). A small
+// per-thread table with round-robin replacement; an entry is only reused on an exact key
+// match, so a freed-and-reallocated buffer at the same address with the same geometry maps
+// to the same (still correct) descriptor.
+struct TmapKey {
+  const void* ptr;
+  long long d[6];
+  bool operator==(const TmapKey& o) const {
+    if (ptr != o.ptr) return false;
+    for (int i = 0; i < 6; ++i)
+      if (d[i] != o.d[i]) return false;
+    return true;
+  }
+};
+
+struct TmapCache {
+  static constexpr int kEntries = 64;
+  TmapKey key[kEntries];
+  CUtensorMap map[kEntries];
+  int used = 0, next = 0;
+  const CUtensorMap* find(const TmapKey& k) const {
+    for (int i = 0; i < used; ++i)
+      if (key[i] == k) return &map[i];
+    return nullptr;
+  }
+  void put(const TmapKey& k, const CUtensorMap& m) {
+    const int i = used < kEntries ? used++ : next;
+    next = (i + 1) % kEntries;
+    key[i] = k;
+    map[i] = m;
+  }
+};
+
+thread_local TmapCache g_tmaps;
+
 // K-major [rows, k] 16-bit matrix, leading dimension `ld` elements, box {64, box_rows}.
 int make_tmap(CUtensorMap* m, const void* ptr, int rows, int k, int ld, int dtype,
               int box_rows) {
+  const TmapKey key{ptr, {0, rows, k, ld, dtype, box_rows}};
+  if (const CUtensorMap* hit = g_tmaps.find(key)) {
+    *m = *hit;
+    return TS_OK;
+  }
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(TS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
@@ -71,6 +122,7 @@ int make_tmap(CUtensorMap* m, const void* ptr, int rows, int k, int ld, int dtyp
   if (r != CUDA_SUCCESS)
     return fail(TS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%d k=%d ld=%d", (int)r,
                 rows, k, ld);
+  g_tmaps.put(key, *m);
   return TS_OK;
 }
 
@@ -100,6 +152,13 @@ EncodeIm2colFn encode_im2col_fn() {
 // is the im2col offset; each load is `pixels` consecutive output pixels x 64 channels.
 int make_tmap_im2col(CUtensorMap* m, const void* ptr, int n, int h, int w, int c, int ldc_px,
                      int dtype, int pixels) {
+  // kind 1 (im2col); n, h, w, c and the pixel stride fully determine the map
+  const TmapKey key{ptr, {1 + (static_cast<long long>(pixels) << 8), n, h, w, c,
+                          static_cast<long long>(ldc_px) * 4 + dtype}};
+  if (const CUtensorMap* hit = g_tmaps.find(key)) {
+    *m = *hit;
+    return TS_OK;
+  }
   EncodeIm2colFn enc = encode_im2col_fn();
   if (!enc) return fail(TS_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable (driver too old?)");
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w),
@@ -118,6 +177,7 @@ int make_tmap_im2col(CUtensorMap* m, const void* ptr, int n, int h, int w, int c
   if (r != CUDA_SUCCESS)
     return fail(TS_ERR_CUDA, "cuTensorMapEncodeIm2col failed (%d) n=%d h=%d w=%d c=%d", (int)r, n,
                 h, w, c);
+  g_tmaps.put(key, *m);
   return TS_OK;
 }
 
@@ -128,98 +188,32 @@ int sm_count() {
   return n;
 }
 
-// Per-device launch preparation of one kernel instantiation, done once per device: the
-// dynamic shared-memory opt-in (a per-device function attribute) and the number of
-// clusters the device can hold at once (a GPC whose SM count is not a multiple of the
-// cluster size leaves SMs idle; 0 = unknown).
-template <int BN, int CG, typename T, bool SW, bool QD>
-int prepare(int* max_clusters) {
-  using C = ts::Cfg<BN, CG, SW, QD>;
-  constexpr int kCluster = CG * (QD ? 2 : 1);
-  constexpr int kMaxDev = 64;
-  static std::atomic<int> done[kMaxDev];
-  static std::atomic<int> mcs[kMaxDev];
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  if (dev < 0 || dev >= kMaxDev) return fail(TS_ERR_CUDA, "device ordinal %d unsupported", dev);
-  if (done[dev].load(std::memory_order_acquire) == 0) {
-    auto kern = ts::chain_kernel<BN, CG, T, SW, QD>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    int mc = 0;
-    if (kCluster > 1) {
-      int sms = 0;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(sms - sms % kCluster, 1, 1);
-      cfg.blockDim = dim3(C::kThreads, 1, 1);
-      cfg.dynamicSmemBytes = C::kSmemBytes;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = kCluster;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess) {
-        (void)cudaGetLastError();
-        mc = 0;
-      }
-    }
-    mcs[dev].store(mc, std::memory_order_relaxed);
-    done[dev].store(1, std::memory_order_release);
-  }
-  *max_clusters = mcs[dev].load(std::memory_order_relaxed);
-  return TS_OK;
-}
-
-// `units` = work items in flight at once: CTAs (CG=1), CTA pairs (CG=2) or two-pair
-// clusters (QD), capped at the co-resident cluster count so every launched cluster runs
-// from the start of the persistent kernel.
-template <int BN, int CG, typename T, bool SW = false, bool QD = false>
-int launch_one(const ts::ChainParams& p, int units, cudaStream_t stream) {
-  using C = ts::Cfg<BN, CG, SW, QD>;
-  constexpr int kCluster = CG * (QD ? 2 : 1);
-  int mc = 0;
-  int r = prepare<BN, CG, T, SW, QD>(&mc);
-  if (r) return r;
-  if (mc > 0 && units > mc) units = mc;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(units * kCluster, 1, 1);
-  cfg.blockDim = dim3(C::kThreads, 1, 1);
-  cfg.dynamicSmemBytes = C::kSmemBytes;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, ts::chain_kernel<BN, CG, T, SW, QD>, p);
-  if (e == cudaSuccess) e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "chain_kernel launch");
-  return TS_OK;
-}
-
-template <int CG, typename T>
-int launch_bn(int bn, const ts::ChainParams& p, int units, cudaStream_t s) {
+template <typename T>
+int launch_bn1(int bn, const ts::ChainParams& p, int units, cudaStream_t s) {
   switch (bn) {
-    case 64: return launch_one<64, CG, T>(p, units, s);
-    case 128: return launch_one<128, CG, T>(p, units, s);
-    case 256: return launch_one<256, CG, T>(p, units, s);
+    case 64: return launch_one<64, 1, T, false, false>(p, units, s);
+    case 128: return launch_one<128, 1, T, false, false>(p, units, s);
+    case 256: return launch_one<256, 1, T, false, false>(p, units, s);
   }
   return fail(TS_ERR_VALUE, "tile_n must be 64, 128 or 256 (got %d)", bn);
 }
 
 template <typename T>
+int launch_bn2(int bn, const ts::ChainParams& p, int units, cudaStream_t s) {
+  switch (bn) {
+    case 128: return launch_one<128, 2, T, false, false>(p, units, s);
+    case 256: return launch_one<256, 2, T, false, false>(p, units, s);
+  }
+  return fail(TS_ERR_VALUE, "cta_group 2 needs tile_n 128 or 256 (got %d)", bn);
+}
+
+template <typename T>
 int launch_swapped(int bn, const ts::ChainParams& p, int units, cudaStream_t s) {
   switch (bn) {
-    case 32: return launch_one<32, 1, T, true>(p, units, s);
-    case 64: return launch_one<64, 1, T, true>(p, units, s);
-    case 128: return launch_one<128, 1, T, true>(p, units, s);
-    case 256: return launch_one<256, 1, T, true>(p, units, s);
+    case 32: return launch_one<32, 1, T, true, false>(p, units, s);
+    case 64: return launch_one<64, 1, T, true, false>(p, units, s);
+    case 128: return launch_one<128, 1, T, true, false>(p, units, s);
+    case 256: return launch_one<256, 1, T, true, false>(p, units, s);
   }
   return fail(TS_ERR_VALUE, "swapped tile_n must be 32, 64, 128 or 256 (got %d)", bn);
 }
@@ -236,11 +230,11 @@ int launch_dispatch(int bn, int cg, int swap, int dtype, const ts::ChainParams& 
   }
   if (cg == 2) {
     if (bn == 64) return fail(TS_ERR_VALUE, "cta_group 2 needs tile_n >= 128");
-    return dtype == TS_DTYPE_BF16 ? launch_bn<2, __nv_bfloat16>(bn, p, units, s)
-                                  : launch_bn<2, __half>(bn, p, units, s);
+    return dtype == TS_DTYPE_BF16 ? launch_bn2<__nv_bfloat16>(bn, p, units, s)
+                                  : launch_bn2<__half>(bn, p, units, s);
   }
-  return dtype == TS_DTYPE_BF16 ? launch_bn<1, __nv_bfloat16>(bn, p, units, s)
-                                : launch_bn<1, __half>(bn, p, units, s);
+  return dtype == TS_DTYPE_BF16 ? launch_bn1<__nv_bfloat16>(bn, p, units, s)
+                                : launch_bn1<__half>(bn, p, units, s);
 }
 
 int tile_n_of(const ts_chain_desc* d) { return d->tile_n == 0 ? 256 : d->tile_n; }
@@ -727,7 +721,7 @@ extern "C" {
 
 int ts_abi_version(void) { return TS_ABI_VERSION; }
 
-const char* ts_last_error(void) { return g_err.c_str(); }
+const char* ts_last_error(void) { return ts_host::g_err.c_str(); }
 
 int ts_sem_count(int policy, int param, int gx, int gy, int gz, int* out) {
   if (gx < 1 || gy < 1 || gz < 1) return fail(TS_ERR_VALUE, "grid dimensions must be >= 1");

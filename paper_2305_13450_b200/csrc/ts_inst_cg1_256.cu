@@ -1,0 +1,5 @@
+// Kernel instantiations (see ts_launch.h).
+#include "ts_launch_impl.cuh"
+
+TS_INSTANTIATE(256, 1, __half, false, false)
+TS_INSTANTIATE(256, 1, __nv_bfloat16, false, false)

@@ -1,0 +1,4 @@
+// Kernel instantiations (see ts_launch.h).
+#include "ts_launch_impl.cuh"
+
+TS_INSTANTIATE(256, 2, __nv_bfloat16, false, false)

@@ -432,6 +432,52 @@ __device__ __forceinline__ void umma_f16_kblock(uint32_t d_tmem, uint64_t adesc,
   }
 }
 
+// One 64-wide K-block into TWO accumulators, interleaved: d0 += A * B0^T and d1 += A * B1^T
+// one 16-deep sub-step at a time, so consecutive MMAs never target the same accumulator.
+// Back-to-back MMAs into one accumulator serialize on its read-modify-write (measured,
+// scripts/mma_rate.cu: 141 cycles per M=128 N=256 MMA against a 128-cycle floor, 91 cycles
+// for N<=128); alternating accumulators issue at the floor.
+template <int CG>
+__device__ __forceinline__ void umma_f16_kblock2(uint32_t d0, uint32_t d1, uint64_t adesc,
+                                                 uint64_t b0, uint64_t b1, uint32_t idesc,
+                                                 uint32_t acc0) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "{\n\t.reg .pred p, t;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "setp.eq.b32 t, %6, %6;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, p;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%1], %2, %4, %5, p;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %7, %8, %5, t;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%1], %7, %9, %5, t;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %10, %11, %5, t;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%1], %10, %12, %5, t;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %13, %14, %5, t;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%1], %13, %15, %5, t;\n\t}" ::"r"(d0),
+        "r"(d1), "l"(adesc), "l"(b0), "l"(b1), "r"(idesc), "r"(acc0), "l"(adesc + 2),
+        "l"(b0 + 2), "l"(b1 + 2), "l"(adesc + 4), "l"(b0 + 4), "l"(b1 + 4), "l"(adesc + 6),
+        "l"(b0 + 6), "l"(b1 + 6)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, t;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "setp.eq.b32 t, %6, %6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %2, %4, %5, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %8, %5, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %7, %9, %5, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %10, %11, %5, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %10, %12, %5, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %13, %14, %5, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %13, %15, %5, t;\n\t}" ::"r"(d0),
+        "r"(d1), "l"(adesc), "l"(b0), "l"(b1), "r"(idesc), "r"(acc0), "l"(adesc + 2),
+        "l"(b0 + 2), "l"(b1 + 2), "l"(adesc + 4), "l"(b0 + 4), "l"(b1 + 4), "l"(adesc + 6),
+        "l"(b0 + 6), "l"(b1 + 6)
+        : "memory");
+  }
+}
+
 // Four K=16 sub-steps of one K-block into four (possibly different) accumulators
 // d0..d3 with per-sub-step accumulate flags, in one issue sequence (single CTA).
 __device__ __forceinline__ void umma_f16_kblock4(uint32_t d0, uint32_t d1, uint32_t d2,
@@ -473,6 +519,17 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)
         "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
         "=r"(r[31])
+      : "r"(taddr));
+}
+
+// 32 lanes x 16 columns of 32-bit: thread i receives TMEM lane (base+i), 16 columns.
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
 

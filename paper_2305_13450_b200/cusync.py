@@ -228,13 +228,16 @@ class CuSync:
             tiles = st.grid.x * st.grid.y
             st.ws = torch.empty(tiles * tail[1] * self.tile_m * st.width, dtype=torch.float32,
                                 device=a.device)
-            st.cnt = torch.zeros(tiles * self.ctas_per_tile, dtype=torch.int32, device=a.device)
+            st.cnt = torch.zeros(2 * tiles * self.ctas_per_tile, dtype=torch.int32,
+                                 device=a.device)
         if splits > 1:
-            # fp32 partials [tile][slice][tile_m rows][width] and per-(tile, CTA) counters
+            # fp32 partials [tile][slice][tile_m rows][width] and per-(tile, CTA) arrival
+            # and partial-ready counters
             tiles = st.grid.x * st.grid.y
             st.ws = torch.empty(tiles * splits * self.tile_m * st.width, dtype=torch.float32,
                                 device=a.device)
-            st.cnt = torch.zeros(tiles * self.ctas_per_tile, dtype=torch.int32, device=a.device)
+            st.cnt = torch.zeros(2 * tiles * self.ctas_per_tile, dtype=torch.int32,
+                                 device=a.device)
         self.stages.append(st)
         self.device = a.device
         self._desc = None
@@ -290,7 +293,7 @@ class CuSync:
             tiles = st.grid.x * st.grid.y
             st.ws = torch.empty(tiles * splits * self.tile_m * st.width, dtype=torch.float32,
                                 device=x.device)
-            st.cnt = torch.zeros(tiles * self.cta_group, dtype=torch.int32, device=x.device)
+            st.cnt = torch.zeros(2 * tiles * self.cta_group, dtype=torch.int32, device=x.device)
         self.stages.append(st)
         self.device = x.device
         self._desc = None

@@ -74,9 +74,11 @@ def report(name, m, n, k, us, clk, pw, err=None):
           f"{pw:4.0f} W  {per_clk:5.0f} MAC/clk/SM ({per_clk / 4096:.1%}){e}", flush=True)
 
 
-def make_stage(x, w, c, tn, cg, band, flags=0):
-    """tn = 512: a double-width CTA-pair stage of a tile_n = 256 chain."""
-    cs = ts.CuSync(tile_n=min(tn, 256), cta_group=cg, mode="stream", extra_flags=flags)
+def make_stage(x, w, c, tn, cg, band, flags=0, qd=1):
+    """tn = 512: a double-width CTA-pair stage of a tile_n = 256 chain (qd = 2: on a
+    two-pair cluster)."""
+    cs = ts.CuSync(tile_n=min(tn, 256), cta_group=cg, mode="stream", extra_flags=flags,
+                   cluster_pairs=qd)
     order = ts.BandedColumnMajor(band) if band > 1 else ts.RowMajor()
     cs.stage(x, w, c, order=order, tile_n=tn if tn > 256 else 0)
     return cs
@@ -110,17 +112,17 @@ def main():
         ref = (x.float() @ w.float().t())
         print(f"M={m} N={n} K={k}", flush=True)
         report("cublas", m, n, k, *time_fn(lambda: torch.matmul(x, w.t(), out=c)))
-        for (tn, cg) in ((512, 2), (256, 2), (256, 1)):
+        for (tn, cg, qd) in ((512, 2, 1), (512, 2, 2), (256, 2, 1), (256, 1, 1)):
             for band in (1, 4):
-                for gbits in ((1, 2) if band == 1 else (0,)):
+                for gbits in ((1,) if band == 1 else (0,)):
                     if band * 128 * cg > m and band > 1:
                         continue
-                    cs = make_stage(x, w, c, tn, cg, band, flags=gbits << 17)
+                    cs = make_stage(x, w, c, tn, cg, band, flags=gbits << 17, qd=qd)
                     cs()
                     torch.cuda.synchronize()
                     err = (c.float() - ref).abs().max().item()
                     grp = {0: 2, 1: 1, 2: 2, 3: 4}[gbits]
-                    report(f"ours {128 * cg}x{tn} band{band} G{grp}", m, n, k, *time_fn(cs),
+                    report(f"ours {128 * cg}x{tn} qd{qd} band{band} G{grp}", m, n, k, *time_fn(cs),
                            err=err)
 
 
