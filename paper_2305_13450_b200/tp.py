@@ -15,8 +15,10 @@ from typing import Callable
 import torch
 import torch.distributed as dist
 
-from .chains import MlpChain
-from .policies import RowSync, SyncPolicy
+from .chains import AttentionChain, MlpChain, SwigluChain, interleave_gate_up
+from .policies import RowSync, SyncPolicy, TileSync
+
+HEAD_DIM = 128  # GPT-3 head width
 
 
 def shard_rows(w: torch.Tensor, rank: int, world: int) -> torch.Tensor:
@@ -42,7 +44,92 @@ def shard_mlp(w1: torch.Tensor, w2: torch.Tensor, rank: int, world: int):
     return shard_rows(w1, rank, world), shard_cols(w2, rank, world)
 
 
-class TPMlp:
+def shard_attention(w_qkv: torch.Tensor, w2: torch.Tensor, rank: int, world: int,
+                    head_dim: int = HEAD_DIM):
+    """Megatron attention shard: this rank's heads of Q, K and V (column-parallel QKV)
+    and the matching input columns of the output projection (row-parallel).
+
+    ``w_qkv`` is [3 * heads * head_dim, H] laid out [Q h0..h(n-1) | K ... | V ...] as the
+    chain reads it (the StridedSync stride is the per-rank head count,
+    reference workloads.py:112-114); the shard keeps that layout over the rank's heads
+    [rank * heads/world, (rank+1) * heads/world). ``w2`` is [H, heads * head_dim]."""
+    n3, hdim = w_qkv.shape
+    if n3 % (3 * head_dim):
+        raise ValueError(f"QKV rows {n3} are not 3 x heads x {head_dim}")
+    heads = n3 // (3 * head_dim)
+    if heads % world:
+        raise ValueError(f"{heads} heads do not split over {world} ranks")
+    if w2.shape[1] != heads * head_dim:
+        raise ValueError(f"output projection has {w2.shape[1]} input columns, "
+                         f"expected {heads * head_dim}")
+    per = heads // world
+    lo, hi = rank * per * head_dim, (rank + 1) * per * head_dim
+    qkv = w_qkv.reshape(3, heads * head_dim, hdim)[:, lo:hi].reshape(3 * (hi - lo), hdim)
+    return qkv.contiguous(), w2[:, lo:hi].contiguous()
+
+
+def shard_swiglu(w_gate: torch.Tensor, w_up: torch.Tensor, w_down: torch.Tensor, rank: int,
+                 world: int, tile_n: int | None = 256):
+    """Megatron SwiGLU shard: this rank's rows of the gate and up projections
+    (column-parallel), packed gate/up-interleaved per ``tile_n`` rows so one producer tile's
+    accumulator holds matching gate and up columns (``interleave_gate_up``; ``tile_n=None``
+    returns the two shards unpacked), and the matching input columns of the down
+    projection (row-parallel). Returns (gate_up [2F/world, H] or (gate, up),
+    down [H, F/world])."""
+    g, u = shard_rows(w_gate, rank, world), shard_rows(w_up, rank, world)
+    d = shard_cols(w_down, rank, world)
+    if tile_n is None:
+        return (g, u), d
+    return interleave_gate_up(g, u, tile_n), d
+
+
+class _TPBase:
+    """Local chain -> all-reduce(sum) of the row-parallel output over the group."""
+
+    group = None
+    local: Callable[[], torch.Tensor]
+
+    def __call__(self) -> torch.Tensor:
+        y = self.local()
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(y, op=dist.ReduceOp.SUM, group=self.group)
+        return y
+
+
+class TPAttention(_TPBase):
+    """One rank of a tensor-parallel GPT-3 attention block: the rank's
+    heads through QKV GeMM -> softmax-dot -> output GeMM as one fused chain
+    (``AttentionChain``: StridedSync(heads per rank) then ``second_policy``), then the
+    single all-reduce(sum) of Y[S, H]. Takes the rank's shards (``shard_attention``);
+    `local` is injectable for CPU (gloo) tests."""
+
+    def __init__(self, x: torch.Tensor, w_qkv_shard: torch.Tensor, w2_shard: torch.Tensor,
+                 group=None, second_policy: SyncPolicy = TileSync(),
+                 local: Callable[[], torch.Tensor] | None = None, **chain_kw):
+        self.group = group
+        if local is None:
+            self.chain = AttentionChain(x, w_qkv_shard, w2_shard, second_policy=second_policy,
+                                        **chain_kw)
+            local = self.chain
+        self.local = local
+
+
+class TPSwiglu(_TPBase):
+    """One rank of a tensor-parallel LLaMA SwiGLU MLP (BASELINE.json configs[3]): the
+    rank's interleaved gate/up shard -> SiLU(g) * u -> down shard as one fused chain
+    (``SwigluChain``), then all-reduce(sum) of Y[B, H]. Shards from ``shard_swiglu``."""
+
+    def __init__(self, x: torch.Tensor, w_gate_up_shard: torch.Tensor,
+                 w_down_shard: torch.Tensor, group=None, policy: SyncPolicy = RowSync(),
+                 local: Callable[[], torch.Tensor] | None = None, **chain_kw):
+        self.group = group
+        if local is None:
+            self.chain = SwigluChain(x, w_gate_up_shard, w_down_shard, policy=policy, **chain_kw)
+            local = self.chain
+        self.local = local
+
+
+class TPMlp(_TPBase):
     """One rank of a tensor-parallel MLP: local fused chain, then all-reduce(sum).
 
     `local` computes this rank's partial output from its weight shards; it defaults to
@@ -58,12 +145,6 @@ class TPMlp:
             self.chain = MlpChain(x, w1_shard, w2_shard, policy=policy, **chain_kw)
             local = self.chain
         self.local = local
-
-    def __call__(self) -> torch.Tensor:
-        y = self.local()
-        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
-            dist.all_reduce(y, op=dist.ReduceOp.SUM, group=self.group)
-        return y
 
 
 class FusedTPMlp:
