@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 5
+#define TS_ABI_VERSION 6
 
 /* ---- status codes ---------------------------------------------------------------- */
 typedef enum {
@@ -108,7 +108,10 @@ typedef enum {
 
 typedef enum {
   TS_MODE_STREAM = 0, /* one launch per stage on one stream, no semaphores (baseline) */
-  TS_MODE_FUSED = 1   /* one persistent launch over all stages' tiles, semaphores     */
+  TS_MODE_FUSED = 1,  /* one persistent launch over all stages' tiles, semaphores     */
+  TS_MODE_CORESIDENT = 2 /* the paper's own form: one launch per stage,
+                            each on its own stream, semaphores live, the consumer stage's
+                            stream gated by the wait kernel — ts_chain_launch_coresident */
 } ts_mode;
 
 typedef enum {
@@ -245,10 +248,13 @@ typedef struct {
                         waits are those of the 256 x 512 tile. */
 } ts_chain_desc;
 
-#define TS_SCRATCH_INTS 16
+#define TS_SCRATCH_INTS 32
 /* scratch layout: [0] work counter, [1] CTA exit counter, [2] trace count,
  *                 [3] watchdog flag (1 = a wait timed out), [4] dot claim counter,
- *                 [8 + d] producer posts of dependency d (done watermark), rest reserved */
+ *                 [8 + d] producer posts of dependency d (done watermark),
+ *                 [16 + 4 s + {0, 1, 2}] co-resident mode: stage s's work counter, exit
+ *                 counter and started flag (set by every CTA of the stage's launch at
+ *                 start — stage.start(); the wait kernel spins on it), rest reserved */
 
 /* Device trace record (one event of the reference's JSONL schema, engine.py:220-248). */
 typedef struct {
@@ -279,6 +285,23 @@ int ts_chain_grid(const ts_chain_desc* desc, int s, int* gx, int* gy);
 /* Paper's wait kernel: one thread on `stream` spins until every
  * flags[i] != 0 (each set by the producer's stage.start()). */
 int ts_wait_kernel_launch(const int* flags, int n, void* stream);
+
+/* The paper's co-resident form (reference engine Mode.FINE with its
+ * scheduling gate, engine.py:173-204): desc->mode must be TS_MODE_CORESIDENT. Stage s
+ * runs as its own launch on streams[s] (n_streams == desc->n_stages) over its tiles in
+ * its tile order, with live semaphores (wait before the dependent A loads, post after the
+ * stores). wait_kernel: 0 = off, 1 = on, 2 = auto (avoid_wait_kernel: skipped when the
+ * producer's and the consumer's launch grids fit one wave together); when on, the
+ * consumer stage's stream first runs ts_wait_kernel_launch on the started flags of its
+ * producers (scratch layout above). launch_order: 0 = stage order, 1 = adversarial
+ * (consumers enqueued before their producers: with the gate off and a consumer grid that
+ * fills the GPU this deadlocks; the semaphore watchdog aborts it after ~4 s and sets
+ * scratch[3]). grid: CTAs (CTA pairs for cta_group 2) per stage launch, NULL = one per
+ * tile (the reference's one thread block per tile; a CTA that finds no tile left exits).
+ * The caller orders the streams against each other across launches (each stage stream
+ * waits for the previous launch to finish). */
+int ts_chain_launch_coresident(const ts_chain_desc* desc, void* const* streams, int n_streams,
+                               int wait_kernel, int launch_order, const int* grid);
 
 /* Stream-ordered semaphore ops for overlapping copies with a chain (the paper's
  * producer -> consumer tile signal, with a copy engine on one side). Both run on the

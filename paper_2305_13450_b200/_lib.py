@@ -22,13 +22,13 @@ TS_POLICY_TILE, TS_POLICY_ROW, TS_POLICY_STRIDED, TS_POLICY_CONV2D = range(4)
 TS_ORDER_ROW_MAJOR, TS_ORDER_STRIDED_ROW_MAJOR, TS_ORDER_BANDED_COLUMN_MAJOR = range(3)
 TS_DTYPE_F16, TS_DTYPE_BF16 = range(2)
 TS_EPI_NONE, TS_EPI_GELU, TS_EPI_SWIGLU, TS_EPI_RELU = range(4)
-TS_MODE_STREAM, TS_MODE_FUSED = range(2)
+TS_MODE_STREAM, TS_MODE_FUSED, TS_MODE_CORESIDENT = range(3)
 TS_STAGE_GEMM, TS_STAGE_ATTN_DOT, TS_STAGE_CONV2D, TS_STAGE_ALLREDUCE = range(4)
 TS_FLAG_KEEP_SEMS, TS_FLAG_NO_REORDER, TS_FLAG_NO_WATCHDOG, TS_FLAG_ROW_INTERLEAVE = 1, 2, 4, 8
 
 TS_MAX_STAGES = 4
 TS_MAX_DEPS = 4
-TS_SCRATCH_INTS = 16
+TS_SCRATCH_INTS = 32
 TS_MAX_PEERS = 8
 
 # Every symbol include/tilesync.h declares (checked by tests/test_abi.py).
@@ -37,6 +37,7 @@ EXPORTS = (
     "ts_consumer_wait", "ts_wait_steps", "ts_order_tile", "ts_avoid_wait_kernel",
     "ts_chain_launch", "ts_chain_grid", "ts_wait_kernel_launch",
     "ts_device_sm_count", "ts_stream_signal", "ts_stream_wait", "ts_chain_units",
+    "ts_chain_launch_coresident",
 )
 
 
@@ -126,12 +127,14 @@ def load() -> ctypes.CDLL:
         "ts_chain_units": ([i, i, i, i, i, ip], i),
         "ts_stream_signal": ([ctypes.c_void_p, i, ctypes.c_void_p], i),
         "ts_stream_wait": ([ctypes.c_void_p, i, ctypes.c_void_p], i),
+        "ts_chain_launch_coresident": ([ctypes.POINTER(ChainDesc),
+                                        ctypes.POINTER(ctypes.c_void_p), i, i, i, ip], i),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.ts_abi_version() != 5:
+    if lib.ts_abi_version() != 6:
         raise RuntimeError("libtilesync_b200.so ABI version mismatch")
     _lib = lib
     return lib

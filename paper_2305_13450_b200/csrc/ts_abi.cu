@@ -295,13 +295,15 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     return fail(TS_ERR_CONFIG, "n_stages must be in [1, %d]", TS_MAX_STAGES);
   if (d->n_deps < 0 || d->n_deps > TS_MAX_DEPS)
     return fail(TS_ERR_CONFIG, "n_deps must be in [0, %d]", TS_MAX_DEPS);
-  if (d->mode != TS_MODE_STREAM && d->mode != TS_MODE_FUSED)
+  if (d->mode != TS_MODE_STREAM && d->mode != TS_MODE_FUSED && d->mode != TS_MODE_CORESIDENT)
     return fail(TS_ERR_CONFIG, "unknown mode %d", d->mode);
   std::memset(p, 0, sizeof(*p));
   p->n_stages = d->n_stages;
   p->n_deps = d->n_deps;
   p->flags = d->flags;
   p->scratch = d->scratch;
+  p->ctl = d->scratch;
+  p->coresident = 0;
   p->trace = static_cast<ts_trace_rec*>(d->trace);
   p->trace_cap = d->trace ? d->trace_cap : 0;
   const int dtype = d->stages[0].dtype;
@@ -563,7 +565,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
         return fail(TS_ERR_CONFIG, "dependency %d: the allreduce stage waits tile by tile (TileSync)", i);
       if (ps.kind != ts::kStageGemm)
         return fail(TS_ERR_CONFIG, "dependency %d: the allreduce producer must be a GeMM", i);
-      if (d->mode == TS_MODE_FUSED && dd.sem == nullptr)
+      if (d->mode != TS_MODE_STREAM && dd.sem == nullptr)
         return fail(TS_ERR_VALUE, "dependency %d: null semaphore array", i);
       if (d->peers->sems[d->peers->rank] != dd.sem)
         return fail(TS_ERR_VALUE, "dependency %d: peers.sems[rank] must be this dependency's semaphores", i);
@@ -577,6 +579,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       dp.kb_per_kstep = 1;
       dp.sem_n = ts::sem_count(dd.policy, dd.param, pg);
       dp.consumer = dd.consumer;
+      dp.producer = dd.producer;
       dp.posts = pg.x * pg.y * pg.z;
       cs.in_dep = i;
       ts::StageParams& pw = p->st[dd.producer];
@@ -620,7 +623,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     }
     if (dd.policy == ts::kTile && k_steps > ps.grid_y)
       return fail(TS_ERR_CONFIG, "dependency %d: tile sync needs one producer column per consumer k-step (%d > %d)", i, k_steps, ps.grid_y);
-    if (d->mode == TS_MODE_FUSED && dd.sem == nullptr)
+    if (d->mode != TS_MODE_STREAM && dd.sem == nullptr)
       return fail(TS_ERR_VALUE, "dependency %d: null semaphore array", i);
     ts::DepParams& dp = p->dep[i];
     dp.sem = dd.sem;
@@ -632,6 +635,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     dp.kb_per_kstep = kb_per_kstep;
     dp.sem_n = ts::sem_count(dd.policy, dd.param, pg);
     dp.consumer = dd.consumer;
+    dp.producer = dd.producer;
     dp.posts = pg.x * pg.y * pg.z;
     cs.in_dep = i;
     ts::StageParams& pw = p->st[dd.producer];
@@ -713,6 +717,11 @@ __global__ void wait_kernel(const int* flags, int n) {
   for (int i = 0; i < n; ++i) {
     while (ts::ptx::ld_acquire_gpu(flags + i) == 0) __nanosleep(100);
   }
+}
+
+// one producer's started flag (co-resident launches): flags are scattered in scratch
+__global__ void wait_kernel_one(const int* flag) {
+  while (ts::ptx::ld_acquire_gpu(flag) == 0) __nanosleep(100);
 }
 
 }  // namespace
@@ -816,6 +825,8 @@ int ts_chain_grid(const ts_chain_desc* desc, int s, int* gx, int* gy) {
 
 int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
   static thread_local ts::ChainParams p;
+  if (desc != nullptr && desc->mode == TS_MODE_CORESIDENT)
+    return fail(TS_ERR_CONFIG, "co-resident chains launch through ts_chain_launch_coresident");
   int r = build_params(desc, &p, true);
   if (r) return r;
   if (desc->scratch == nullptr) return fail(TS_ERR_VALUE, "null scratch buffer");
@@ -869,6 +880,65 @@ int ts_wait_kernel_launch(const int* flags, int n, void* stream) {
   wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flags, n);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_fail(e, "wait_kernel launch");
+}
+
+int ts_chain_launch_coresident(const ts_chain_desc* desc, void* const* streams, int n_streams,
+                               int wait_kernel, int launch_order, const int* grid) {
+  static thread_local ts::ChainParams p;
+  if (desc == nullptr || streams == nullptr) return fail(TS_ERR_VALUE, "null descriptor or streams");
+  if (desc->mode != TS_MODE_CORESIDENT)
+    return fail(TS_ERR_CONFIG, "ts_chain_launch_coresident needs mode TS_MODE_CORESIDENT");
+  if (wait_kernel < 0 || wait_kernel > 2) return fail(TS_ERR_VALUE, "wait_kernel must be 0, 1 or 2");
+  int r = build_params(desc, &p, true);
+  if (r) return r;
+  if (desc->scratch == nullptr) return fail(TS_ERR_VALUE, "null scratch buffer");
+  if (n_streams != p.n_stages)
+    return fail(TS_ERR_VALUE, "%d streams for %d stages", n_streams, p.n_stages);
+  if (desc->flags & TS_FLAG_ROW_INTERLEAVE)
+    return fail(TS_ERR_CONFIG, "row interleaving is a fused-mode claim order");
+  for (int s = 0; s < p.n_stages; ++s) {
+    if (p.st[s].kind == ts::kStageAllReduce)
+      return fail(TS_ERR_CONFIG, "the all-reduce stage runs in fused or stream mode only");
+    if (streams[s] == nullptr) return fail(TS_ERR_VALUE, "null stream for stage %d", s);
+  }
+  const int bn = tile_n_of(desc);
+  const int cg = cta_group_of(desc);
+  const int np = cluster_pairs_of(desc);
+  const int dtype = desc->stages[0].dtype;
+  int sms = sm_count();
+  if (sms <= 0) return fail(TS_ERR_CUDA, "could not query the SM count");
+  const int units = sms / (cg * np);  // one CTA (pair, cluster) per SM: occupancy 1
+  int g[TS_MAX_STAGES];
+  for (int s = 0; s < p.n_stages; ++s) {
+    const int tiles = p.st[s].item_end - p.st[s].item_begin;
+    g[s] = grid != nullptr && grid[s] > 0 ? (grid[s] < tiles ? grid[s] : tiles) : tiles;
+  }
+  for (int i = 0; i < p.n_stages; ++i) {
+    const int s = launch_order ? p.n_stages - 1 - i : i;
+    cudaStream_t st = static_cast<cudaStream_t>(streams[s]);
+    // the reference's gate (engine.gated_producers): hold this stage back until every
+    // producer it depends on has started, unless "auto" finds both grids fit one wave
+    int flags_at[TS_MAX_DEPS], nf = 0;
+    for (int d = 0; d < p.n_deps && wait_kernel != 0; ++d) {
+      if (p.dep[d].consumer != s) continue;
+      const int pr = p.dep[d].producer;
+      if (wait_kernel == 2 && ts::avoid_wait_kernel(g[pr], 1, g[s], 1, units)) continue;
+      flags_at[nf++] = ts::kCtlBase + ts::kCtlInts * pr + 2;
+    }
+    for (int f = 0; f < nf; ++f) {
+      wait_kernel_one<<<1, 1, 0, st>>>(desc->scratch + flags_at[f]);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return cuda_fail(e, "wait_kernel launch");
+    }
+    ts::ChainParams q = p;
+    q.item_lo = q.st[s].item_begin;
+    q.item_hi = q.st[s].item_end;
+    q.ctl = desc->scratch + ts::kCtlBase + ts::kCtlInts * s;
+    q.coresident = 1;
+    r = launch_dispatch(bn, cg, desc->swap_ab, dtype, q, g[s], st, np);
+    if (r) return r;
+  }
+  return TS_OK;
 }
 
 int ts_stream_signal(int* sem, int value, void* stream) {

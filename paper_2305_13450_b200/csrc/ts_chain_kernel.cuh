@@ -120,6 +120,7 @@ struct DepParams {
   int kb_per_kstep;     // consumer K-blocks per reference k-step
   int sem_n;
   int consumer;         // consumer stage index
+  int producer;         // producer stage index
   int posts;            // producer posts in one launch (grid x*y*z): the done watermark
 };
 
@@ -129,6 +130,11 @@ struct ChainParams {
   int n_stages, n_deps, total_items;
   int item_lo, item_hi;  // this launch claims global items [item_lo, item_hi)
   int* scratch;
+  // this launch's work / exit counters: scratch itself, or (co-resident mode: one launch
+  // per stage on its own stream) the stage's block scratch + kCtlBase + kCtlInts * s,
+  // whose [2] is the stage's "started" flag (stage.start())
+  int* ctl;
+  int coresident;
   ts_trace_rec* trace;
   int trace_cap;
   int flags;
@@ -306,6 +312,10 @@ __device__ __forceinline__ void sem_spin(const ChainParams& p, const int* sem, i
   // relaxed probes with back-off (an acquiring load per probe would invalidate L1 on
   // every iteration), then one acquiring load
   const bool watchdog = (p.flags & TS_FLAG_NO_WATCHDOG) == 0;
+  // once a wait has timed out the launch is void: later waits return at once, so a
+  // deadlocked launch (e.g. a co-resident consumer grid holding every SM) drains in one
+  // watchdog period instead of one per wait
+  if (watchdog && ptx::ld_relaxed_gpu(&p.scratch[3]) != 0) return;
   uint64_t t0 = ptx::global_timer();
   uint32_t ns = 32;
 #pragma unroll 1
@@ -371,6 +381,10 @@ __device__ __forceinline__ void sem_wait(const ChainParams& p, const int* sem, i
 // loaded together with the semaphores, so an unsatisfied watermark costs no extra round
 // trip. Returns true when the watermark was reached.
 constexpr int kDoneBase = 8;
+// co-resident launches: stage s's work counter, exit counter and started flag at
+// scratch[kCtlBase + kCtlInts * s + {0, 1, 2}] (TS_SCRATCH_INTS covers TS_MAX_STAGES)
+constexpr int kCtlBase = 16;
+constexpr int kCtlInts = 4;
 
 __device__ __forceinline__ bool sem_wait_dep(const ChainParams& p, int d, const int* s0, int e0,
                                              const int* s1, int e1, const int* s2, int e2,
@@ -688,6 +702,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       ptx::tma_prefetch_desc(&p.st[s].tmap_b);
     }
   }
+  // stage.start(): a co-resident launch marks its stage as started,
+  // which releases the wait kernel on the consumer stage's stream
+  if (p.coresident && threadIdx.x == 0) atomicExch(&p.ctl[2], 1);
   __syncthreads();  // barrier init (thread 0) before the allocator warp writes tmem_slot
   if (warp == 2) ptx::tmem_alloc<C::kTmemCols, CG>(tmem_slot);
   ptx::tc_fence_before();
@@ -762,7 +779,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         const int slot = it % kTileRing;
         if (uleader) {
           ptx::mbar_wait(&ti_empty[slot], ((it / kTileRing) & 1) ^ 1);  // no data: slot reuse
-          g = p.item_lo + atomicAdd(&p.scratch[0], 1);
+          g = p.item_lo + atomicAdd(&p.ctl[0], 1);
           if (g >= p.item_hi) g = -1;
           ti_item[slot] = g;
           ptx::mbar_arrive(&ti_full[slot]);
@@ -1916,7 +1933,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
   }
   if (threadIdx.x == 0) {
     __threadfence();
-    const int prev = atomicAdd(&p.scratch[1], 1);
+    const int prev = atomicAdd(&p.ctl[1], 1);
     *last_flag = (prev == static_cast<int>(gridDim.x) - 1);
   }
   __syncthreads();
@@ -1935,19 +1952,42 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       if (threadIdx.x == 0) sem_spin_sys(p, p.peers.done[p.peers.rank], p.ar_done * p.peers.epoch);
       __syncthreads();
     }
-    if ((p.flags & TS_FLAG_KEEP_SEMS) == 0) {
+    if (p.coresident) {
+      // One stage per launch: the consumer's launch is the last reader of its incoming
+      // dependencies' semaphores and watermarks, and of its producers' started flags.
+      const int s = stage_of(p, p.item_lo);
       for (int d = 0; d < p.n_deps; ++d) {
-        if (p.st[p.dep[d].consumer].kind == kStageAllReduce) continue;  // epoch-monotone
-        for (int i = threadIdx.x; i < p.dep[d].sem_n; i += C::kThreads) p.dep[d].sem[i] = 0;
+        if (p.dep[d].consumer != s) continue;
+        if ((p.flags & TS_FLAG_KEEP_SEMS) == 0)
+          for (int i = threadIdx.x; i < p.dep[d].sem_n; i += C::kThreads) p.dep[d].sem[i] = 0;
+        if (threadIdx.x == 0) {
+          p.scratch[kDoneBase + d] = 0;
+          p.scratch[kCtlBase + kCtlInts * p.dep[d].producer + 2] = 0;
+        }
       }
+      if (threadIdx.x == 0) {
+        p.ctl[0] = 0;
+        p.ctl[1] = 0;
+        bool waited_on = false;  // nothing consumes this stage: nobody else resets its flag
+        for (int d = 0; d < p.n_deps; ++d) waited_on = waited_on || p.dep[d].producer == s;
+        if (!waited_on) p.ctl[2] = 0;
+      }
+      __threadfence();
+    } else {
+      if ((p.flags & TS_FLAG_KEEP_SEMS) == 0) {
+        for (int d = 0; d < p.n_deps; ++d) {
+          if (p.st[p.dep[d].consumer].kind == kStageAllReduce) continue;  // epoch-monotone
+          for (int i = threadIdx.x; i < p.dep[d].sem_n; i += C::kThreads) p.dep[d].sem[i] = 0;
+        }
+      }
+      if (threadIdx.x == 0) {
+        p.scratch[0] = 0;
+        p.scratch[1] = 0;
+        p.scratch[4] = 0;  // last-arriver dot claim counter
+      }
+      if (threadIdx.x < TS_MAX_DEPS) p.scratch[kDoneBase + threadIdx.x] = 0;  // watermarks
+      __threadfence();
     }
-    if (threadIdx.x == 0) {
-      p.scratch[0] = 0;
-      p.scratch[1] = 0;
-      p.scratch[4] = 0;  // last-arriver dot claim counter
-    }
-    if (threadIdx.x < TS_MAX_DEPS) p.scratch[kDoneBase + threadIdx.x] = 0;  // watermarks
-    __threadfence();
   }
 }
 

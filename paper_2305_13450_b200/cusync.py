@@ -19,6 +19,14 @@ Modes
     order replacing the wait kernel: deadlock-free by construction).
   * ``"stream"`` — the same kernel, one launch per stage on one stream, no semaphores:
     the stream-synchronized baseline the paper compares against.
+  * ``"coresident"`` — the paper's own form: one launch per stage,
+    each on its own stream (producers at higher priority), semaphores live; a consumer
+    stage's stream first runs the one-thread wait kernel on its producers' started flags
+    (``wait_kernel`` = "on" / "off" / "auto", the reference's SimOptions.wait_kernel and
+    gated_producers, engine.py:173-204; ``CuStage.wait_kernel()`` forces it on).
+    ``adversarial=True`` enqueues consumers before producers (SimOptions.adversarial_order):
+    with the gate off a consumer grid that fills the GPU deadlocks, and the semaphore
+    watchdog aborts the launch (``watchdog_fired()``).
 """
 
 from __future__ import annotations
@@ -29,7 +37,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib
-from .engine import Dependency, Event, Mode, Scenario, SimTrace, Stage
+from .engine import Dependency, Event, Mode, Scenario, SimOptions, SimTrace, Stage
 from .errors import ConfigError
 from .gpu import Dim3, GpuConfig
 from .policies import (Conv2DTileSync, RowMajor, SyncPolicy, TileOrder, order_code,
@@ -104,6 +112,13 @@ class CuStage:
     def flops(self) -> int:
         return 0 if self.kind in ("dot", "allreduce") else 2 * self.m * self.n * self.k
 
+    def wait_kernel(self) -> "CuStage":
+        """``stage.wait_kernel()``: in co-resident mode, hold this
+        stage's launch back until its producers have started (the chain's gate becomes
+        "on")."""
+        self.cs.wait_kernel = "on"
+        return self
+
 
 @dataclass
 class CuDep:
@@ -136,13 +151,19 @@ class CuSync:
     # (256 x 512, every GeMM stage tile_n=512) runs as two 256 x 256 pair tiles with
     # double-buffered accumulators (ts_chain_desc.cluster_pairs)
     cluster_pairs: int = 1
+    # co-resident mode only: the scheduling gate and the launch order (SimOptions)
+    wait_kernel: str = "auto"
+    adversarial: bool = False
+    coresident_grid: tuple | None = None  # CTAs (pairs) per stage launch; None = per tile
     device: torch.device | None = None
     stages: list[CuStage] = field(default_factory=list)
     deps: list[CuDep] = field(default_factory=list)
 
     def __post_init__(self) -> None:
-        if self.mode not in ("fused", "stream"):
-            raise ConfigError(f"mode must be 'fused' or 'stream', got {self.mode!r}")
+        if self.mode not in ("fused", "stream", "coresident"):
+            raise ConfigError(f"mode must be 'fused', 'stream' or 'coresident', got {self.mode!r}")
+        if self.wait_kernel not in ("on", "off", "auto"):
+            raise ConfigError(f"wait_kernel must be on/off/auto, got {self.wait_kernel!r}")
         if self.swap_ab:
             if self.tile_n not in (32, 64, 128, 256):
                 raise ConfigError(f"swapped tile_n must be 32, 64, 128 or 256, got {self.tile_n}")
@@ -160,6 +181,7 @@ class CuSync:
         self._scratch: torch.Tensor | None = None
         self._trace: torch.Tensor | None = None
         self._trace_cap = 0
+        self._streams: list | None = None
 
     @property
     def tile_m(self) -> int:
@@ -394,8 +416,10 @@ class CuSync:
                                 order=st.order, operands=operands))
         deps = tuple(Dependency(d.producer.id, d.consumer.id, d.operand, d.policy)
                      for d in self.deps if d.consumer.kind != "allreduce")
-        mode = Mode.FINE if self.mode == "fused" else Mode.STREAM
-        return Scenario(gpu=GpuConfig(num_sms), stages=tuple(stages), deps=deps, mode=mode)
+        mode = Mode.STREAM if self.mode == "stream" else Mode.FINE
+        opts = SimOptions(wait_kernel=self.wait_kernel, adversarial_order=self.adversarial)
+        return Scenario(gpu=GpuConfig(num_sms), stages=tuple(stages), deps=deps, mode=mode,
+                        options=opts)
 
     # -- launch ------------------------------------------------------------------------
     def _build(self) -> _lib.ChainDesc:
@@ -432,7 +456,8 @@ class CuSync:
             dd.operand = 0
             dd.policy, dd.param = policy_code(dep.policy)
             dd.sem = dep.sem.data_ptr()
-        d.mode = _lib.TS_MODE_FUSED if self.mode == "fused" else _lib.TS_MODE_STREAM
+        d.mode = {"fused": _lib.TS_MODE_FUSED, "stream": _lib.TS_MODE_STREAM,
+                  "coresident": _lib.TS_MODE_CORESIDENT}[self.mode]
         d.tile_n = self.tile_n
         d.cta_group = self.cta_group
         d.swap_ab = 1 if self.swap_ab else 0
@@ -480,8 +505,33 @@ class CuSync:
         with torch.cuda.device(self.device):
             if self._trace is not None:
                 self._scratch[2].zero_()
+            if self.mode == "coresident":
+                self._launch_coresident(s)
+                return
             _lib.check(_lib.load().ts_chain_launch(ctypes.byref(self._desc),
                                                    ctypes.c_void_p(s.cuda_stream)))
+
+    def _launch_coresident(self, s: torch.cuda.Stream) -> None:
+        """One launch per stage on its own stream (stage 0 at the highest priority), the
+        stage streams ordered after `s` and `s` after all of them, so consecutive chains
+        never overlap (the semaphores and started flags are reset by the consumers)."""
+        n = len(self.stages)
+        if self._streams is None:
+            lo, hi = torch.cuda.Stream.priority_range()
+            self._streams = [torch.cuda.Stream(device=self.device,
+                                               priority=max(hi, lo - (n - 1 - i)))
+                             for i in range(n)]
+        for st in self._streams:
+            st.wait_stream(s)
+        ptrs = (ctypes.c_void_p * n)(*[st.cuda_stream for st in self._streams])
+        grid = None
+        if self.coresident_grid is not None:
+            grid = (ctypes.c_int * n)(*self.coresident_grid)
+        gate = {"off": 0, "on": 1, "auto": 2}[self.wait_kernel]
+        _lib.check(_lib.load().ts_chain_launch_coresident(
+            ctypes.byref(self._desc), ptrs, n, gate, 1 if self.adversarial else 0, grid))
+        for st in self._streams:
+            s.wait_stream(st)
 
     __call__ = launch
 
@@ -540,7 +590,7 @@ class CuSync:
         return [e[3] for e in evs]
 
     def sim_trace(self) -> SimTrace:
-        mode = Mode.FINE if self.mode == "fused" else Mode.STREAM
+        mode = Mode.STREAM if self.mode == "stream" else Mode.FINE
         return SimTrace(mode=mode, events=self.trace_events(),
                         final_semaphores=self.final_semaphores())
 

@@ -14,7 +14,11 @@ KEYS = [
     ("lts__t_sector_hit_rate.pct", "l2_hit_pct"),
     ("lts__t_sectors_srcunit_tex.sum", "l2_sectors_from_sm"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2_pct"),
-    ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor_pct"),
+    # tcgen05 tensor-pipe activity (the sm_100 raw page names it sm__mem_tensor_*; the
+    # Hopper-era sm__pipe_tensor_cycles_active* names are absent); any other raw metric
+    # mentioning the tensor pipe is listed below the fixed keys
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor_pct_elapsed"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor_pct_active"),
     ("l1tex__m_xbar2l1tex_read_bytes.sum.pct_of_peak_sustained_elapsed", "xbar2sm_pct"),
     ("launch__registers_per_thread", "regs"),
     ("launch__grid_size", "grid"),
@@ -34,6 +38,10 @@ def main(path):
         for key, label in KEYS:
             if key in idx:
                 print(f"  {label:20s} {r[idx[key]]:>16s} {units[idx[key]]}")
+        fixed = {k for k, _ in KEYS}
+        for h, i in idx.items():
+            if h not in fixed and "tensor" in h and "pct" in h and r[i] not in ("", "n/a"):
+                print(f"  {h[:70]:70s} {r[i]:>10s} {units[i]}")
 
 
 if __name__ == "__main__":

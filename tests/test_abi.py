@@ -35,7 +35,7 @@ def test_every_declared_symbol_is_exported():
 
 
 def test_abi_version():
-    assert _lib.load().ts_abi_version() == 5
+    assert _lib.load().ts_abi_version() == 6
 
 
 def test_struct_layout_matches_header(tmp_path):
