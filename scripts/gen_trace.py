@@ -37,6 +37,7 @@ def main():
             kw, _ = planner.pick_mlp(x, w1, w2, mode="fused")
         else:
             kw = json.loads(spec)
+            kw.setdefault("mode", "fused")
             kw["policy"] = POL[kw.get("policy", "row")]
             kw["cons_order"] = order(kw.get("cons_order", "row"))
             if "cons_tail" in kw:

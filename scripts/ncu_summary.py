@@ -40,7 +40,9 @@ def main(path):
                 print(f"  {label:20s} {r[idx[key]]:>16s} {units[idx[key]]}")
         fixed = {k for k, _ in KEYS}
         for h, i in idx.items():
-            if h not in fixed and "tensor" in h and "pct" in h and r[i] not in ("", "n/a"):
+            if (h not in fixed and h.startswith(("sm__pipe_tensor_cycles_active.avg",
+                                                  "sm__pipe_tensor_subpipe_hmma"))
+                    and r[i] not in ("", "n/a")):
                 print(f"  {h[:70]:70s} {r[i]:>10s} {units[i]}")
 
 
