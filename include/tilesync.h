@@ -118,12 +118,27 @@ typedef enum {
   TS_FLAG_KEEP_SEMS = 1,   /* do not zero semaphores at exit (for final-value parity)  */
   TS_FLAG_NO_REORDER = 2,  /* disable "+R": load the dependent A tile before B         */
   TS_FLAG_NO_WATCHDOG = 4, /* spin forever instead of aborting a wait after ~4 s      */
-  TS_FLAG_ROW_INTERLEAVE = 8 /* fused two-GeMM Row/TileSync chains: claim tiles row by
+  TS_FLAG_ROW_INTERLEAVE = 8, /* fused two-GeMM Row/TileSync chains: claim tiles row by
                               row across the stages (producer row r, consumer row r,
                               producer row r+1, ...) instead of stage by stage — for
                               inputs that arrive row by row (MlpChain.run_host); every
                               consumer item is still claimed after the producer items
                               it waits on                                               */
+  TS_FLAG_BALANCED = 16      /* fused CTA-pair 256-wide GeMM chains: static stream-K
+                              schedule. Each stage's flattened (tile in claim order,
+                              K-block) space is cut into one equal range per work unit
+                              (CTA pair); unit u runs its range of every stage in turn,
+                              cut at tile boundaries. A segment that does not start its
+                              tile writes an fp32 partial plane (workspace: fp32[units x 2
+                              x 128 x tile_cols], indexed by unit) and counts it into the
+                              tile half's counter (counters: int32[tiles x 2], zero); the
+                              tile's head segment (K-block 0, the last item of its unit)
+                              waits for those planes, sums them into its TMEM accumulator,
+                              applies the epilogue, stores and posts once — the
+                              reference's semantics of an unsplit tile (z = 1). Every unit
+                              ends each stage within one K-block of the others, so no
+                              wave runs partially filled (the B200 extension to the
+                              paper's per-stage tile counters, engine.py:424-470)       */
 } ts_flags;
 
 typedef struct {

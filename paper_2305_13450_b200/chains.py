@@ -30,11 +30,12 @@ class MlpChain:
                  cons_order: TileOrder = RowMajor(), swap_ab: bool = False,
                  prod_splits: int = 1, cons_splits: int = 1, prod_tile_n: int = 0,
                  cons_tile_n: int = 0, row_interleave: bool = False,
-                 cons_tail: tuple = (0, 1), cluster_pairs: int = 1):
+                 cons_tail: tuple = (0, 1), cluster_pairs: int = 1, balanced: bool = False):
         """``row_interleave`` claims GeMM1 row r, GeMM2 row r, GeMM1 row r+1, ... (fused
         RowSync/TileSync, RowMajor orders): for inputs that arrive row by row
         (``run_host``), a row's GeMM2 tiles are not queued behind later rows' GeMM1 tiles
-        that still wait for their copy."""
+        that still wait for their copy. ``balanced`` runs both GeMMs on the static
+        stream-K schedule (TS_FLAG_BALANCED; CTA-pair 256-wide tiles)."""
         m = x.shape[0]
         self.x, self.w1, self.w2 = x, w1, w2
         self.h = torch.empty(m, w1.shape[0], dtype=x.dtype, device=x.device)
@@ -42,7 +43,7 @@ class MlpChain:
         self.cs = CuSync(tile_n=tile_n, mode=mode, reorder=reorder, keep_sems=keep_sems,
                          num_ctas=num_ctas, extra_flags=extra_flags, cta_group=cta_group,
                          swap_ab=swap_ab, row_interleave=row_interleave,
-                         cluster_pairs=cluster_pairs)
+                         cluster_pairs=cluster_pairs, balanced=balanced)
         self.prod = self.cs.stage(x, w1, self.h, epilogue="gelu", order=prod_order, id="gemm1",
                                   splits=prod_splits, tile_n=prod_tile_n)
         self.cons = self.cs.stage(self.h, w2, self.y, order=cons_order, id="gemm2",

@@ -304,6 +304,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
   p->scratch = d->scratch;
   p->ctl = d->scratch;
   p->coresident = 0;
+  p->balanced = (d->flags & TS_FLAG_BALANCED) ? 1 : 0;
   p->trace = static_cast<ts_trace_rec*>(d->trace);
   p->trace_cap = d->trace ? d->trace_cap : 0;
   const int dtype = d->stages[0].dtype;
@@ -537,6 +538,29 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     }
   }
   p->total_items = items;
+  if (p->balanced) {
+    // static stream-K assignment (see TS_FLAG_BALANCED): GeMM stages of CTA-pair 256-wide
+    // chains whose partial planes are reduced into the head segment's TMEM accumulator
+    if (d->mode != TS_MODE_FUSED)
+      return fail(TS_ERR_CONFIG, "the balanced schedule runs in fused mode");
+    if (cg != 2 || bn != 256 || swap || np != 1)
+      return fail(TS_ERR_CONFIG, "the balanced schedule needs cta_group 2, tile_n 256, one CTA "
+                                 "pair per cluster");
+    if (d->flags & TS_FLAG_ROW_INTERLEAVE)
+      return fail(TS_ERR_CONFIG, "row interleaving is a dynamic claim order");
+    for (int s = 0; s < d->n_stages; ++s) {
+      const ts_stage_desc& st = d->stages[s];
+      const ts::StageParams& sp = p->st[s];
+      if (sp.kind != ts::kStageGemm || sp.splits != 1 || sp.tail_tiles != 0 ||
+          st.epilogue == TS_EPI_SWIGLU)
+        return fail(TS_ERR_CONFIG, "stage %d: the balanced schedule takes unsplit GeMM stages "
+                                   "(no conv / dot / all-reduce, tail or SwiGLU)", s);
+      if (!st.workspace || !st.counters)
+        return fail(TS_ERR_VALUE, "stage %d: the balanced schedule needs a workspace and counters", s);
+      if (sp.k_blocks >= 65536)
+        return fail(TS_ERR_CONFIG, "stage %d: k too large for the balanced schedule", s);
+    }
+  }
   for (int i = 0; i < d->n_deps; ++i) {
     const ts_dep_desc& dd = d->deps[i];
     if (dd.producer < 0 || dd.producer >= d->n_stages || dd.consumer < 0 ||
@@ -842,7 +866,8 @@ int ts_chain_launch(const ts_chain_desc* desc, void* stream) {
   if (desc->mode == TS_MODE_FUSED) {
     p.item_lo = 0;
     p.item_hi = p.total_items;
-    int grid = ctas < p.total_items ? ctas : p.total_items;
+    // balanced: every unit runs (the kernel derives the stream-K widths from its grid)
+    int grid = p.balanced || ctas < p.total_items ? ctas : p.total_items;
     return launch_dispatch(bn, cg, desc->swap_ab, dtype, p, grid, s, np);
   }
   // Stream mode: the same kernel, one launch per stage, no semaphores — the

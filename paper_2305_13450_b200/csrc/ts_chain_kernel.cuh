@@ -135,6 +135,7 @@ struct ChainParams {
   // whose [2] is the stage's "started" flag (stage.start())
   int* ctl;
   int coresident;
+  int balanced;   // TS_FLAG_BALANCED: static stream-K assignment (0 = dynamic claims)
   ts_trace_rec* trace;
   int trace_cap;
   int flags;
@@ -204,7 +205,8 @@ struct Cfg {
   static constexpr int kNumBars = kFullRing + kCommitRing + 4 + 2 * kTileRing + kPeerRing + 2;
   // + tile ring ids, TMEM slot, flags and the last-arriver dot list (64 ints), ring-entry
   // owners (commit group that last read each entry)
-  static constexpr int kSmemBytes = 1024 + kBarOffset + kNumBars * 8 + 64 + 272 + 4 * kRing;
+  static constexpr int kSmemBytes =
+      1024 + kBarOffset + kNumBars * 8 + 64 + 272 + 4 * kRing + 4 * kTileRing + 16;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
   static_assert(kBRows % 8 == 0 && kBRows <= 256, "B box rows");
 };
@@ -517,6 +519,20 @@ struct Tile {
   int z;  // split-K slices of this item's tile (st.splits, or tail_splits for a tail tile)
 };
 
+// Balanced (stream-K) schedule: the stage's flattened (tile in claim order, K-block) space
+// is cut into `units` equal ranges of bal_width K-blocks; unit u runs [u w, (u + 1) w).
+__device__ __forceinline__ int bal_width(const StageParams& st, int units) {
+  const int total = st.grid_x * st.grid_y * st.k_blocks;
+  return (total + units - 1) / units;
+}
+
+// A balanced item is the segment [kb0, kb1) of tile tb (packed (kb0 << 16) | kb1 in the
+// tile ring). Role 0: the whole tile. Role 1 (kb0 > 0, the first item of its unit): writes
+// an fp32 partial plane indexed by its unit and counts it into the tile half's counter; it
+// does not post. Role 2 (the head: kb0 = 0, kb1 < k_blocks, the last item of its unit):
+// waits for the planes of units ua..ub (every range that starts inside the tile), sums
+// them into its TMEM accumulator, applies the epilogue, stores and posts once.
+
 // Split-K slices of item g of stage st (see StageParams::tail_tiles).
 __device__ __forceinline__ int item_slices(const StageParams& st, int tb) {
   if (st.tail_tiles > 0 && tb >= st.grid_x * st.grid_y - st.tail_tiles) return st.tail_splits;
@@ -662,6 +678,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
   int* dot_count = split_flag + 1;  // last-arriver dot tiles released by a post
   int* dot_list = dot_count + 1;    // [0, 32): dot tile columns, [32, 64): their tb
   int* owner = dot_list + 64;       // [R]: commit group that last read each ring entry
+  int* ti_kb = owner + R;           // [kTileRing]: balanced segment K range per ring slot
+  int* bst = ti_kb + kTileRing;     // [3]: balanced scheduler state (stage, next, end)
+  const bool bal = p.balanced != 0;
+  const int unit = static_cast<int>(blockIdx.x) / (CG * NP);  // this CTA's work unit
+  const int units = static_cast<int>(gridDim.x) / (CG * NP);  // all co-resident (host cap)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -717,7 +738,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   // Receive the next tile id from the ring (and release the slot).
-  auto ring_take = [&](int it, bool remote_release) -> int {
+  auto ring_take = [&](int it, bool remote_release, int& kbr) -> int {
     const int slot = it % kTileRing;
     if constexpr (CG == 2) {
       ptx::mbar_wait_cluster(&ti_full[slot], (it / kTileRing) & 1);
@@ -731,9 +752,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
     int g;
     if constexpr (CG == 2) {
       g = lane == 0 ? ti_item[slot] : 0;
+      kbr = lane == 0 ? ti_kb[slot] : 0;
       g = __shfl_sync(0xffffffffu, g, 0);
+      kbr = __shfl_sync(0xffffffffu, kbr, 0);
     } else {
       g = ti_item[slot];
+      kbr = ti_kb[slot];
       __syncwarp();
     }
     if (lane == 0) {
@@ -773,26 +797,67 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         }
         owner[e] = static_cast<int>(cid);
       };
+      // balanced schedule state (shared memory: the scheduler lane's registers are the
+      // kernel's tightest): stage, next and end position in the stage's flattened space
+      if (bal) {
+        bst[0] = 0;
+        bst[1] = -1;
+        bst[2] = 0;
+      }
 #pragma unroll 1
       for (int it = 0;; ++it) {
-        int g;
+        int g, kbr = 0;
         const int slot = it % kTileRing;
         if (uleader) {
           ptx::mbar_wait(&ti_empty[slot], ((it / kTileRing) & 1) ^ 1);  // no data: slot reuse
-          g = p.item_lo + atomicAdd(&p.ctl[0], 1);
-          if (g >= p.item_hi) g = -1;
+          if (bal) {
+            // static stream-K assignment: this unit's K-block range of each stage in turn,
+            // cut at tile boundaries (the first segment may start inside a tile, the last
+            // may end inside one)
+            g = -1;
+            int bs = bst[0], bpos = bst[1], bend = bst[2];
+            while (bs < p.n_stages) {
+              const StageParams& sb = p.st[bs];
+              const int kbs = sb.k_blocks;
+              if (bpos < 0) {
+                const int total = sb.grid_x * sb.grid_y * kbs;
+                const int w = bal_width(sb, units);
+                bpos = unit * w;
+                bend = bpos + w < total ? bpos + w : total;
+              }
+              if (bpos < bend) {
+                const int tile = bpos / kbs, k0 = bpos % kbs;
+                const int k1 = kbs < k0 + (bend - bpos) ? kbs : k0 + (bend - bpos);
+                g = sb.item_begin + tile;
+                kbr = (k0 << 16) | k1;
+                bpos += k1 - k0;
+                break;
+              }
+              ++bs;
+              bpos = -1;
+            }
+            bst[0] = bs;
+            bst[1] = bpos;
+            bst[2] = bend;
+          } else {
+            g = p.item_lo + atomicAdd(&p.ctl[0], 1);
+            if (g >= p.item_hi) g = -1;
+          }
           ti_item[slot] = g;
+          ti_kb[slot] = kbr;
           ptx::mbar_arrive(&ti_full[slot]);
           if constexpr (CG == 2) {
 #pragma unroll
             for (int r = 1; r < NP * CG; ++r) {
               ptx::st_cluster_u32(ptx::mapa(&ti_item[slot], r), static_cast<uint32_t>(g));
+              ptx::st_cluster_u32(ptx::mapa(&ti_kb[slot], r), static_cast<uint32_t>(kbr));
               ptx::mbar_arrive_remote(ptx::mapa(&ti_full[slot], r));
             }
           }
         } else {
           ptx::mbar_wait_cluster(&ti_full[slot], (it / kTileRing) & 1);
           g = ti_item[slot];
+          kbr = ti_kb[slot];
           ptx::mbar_arrive_remote(ptx::mapa(&ti_empty[slot], 0));
         }
         if (g < 0) break;
@@ -819,8 +884,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         const uint64_t pol_a = ah == 1 ? pol_first : (ah == 2 ? pol_normal : pol_last);
         // diagnostic only (flag bit 12): time the chain without semaphore waits
         const bool no_wait = (p.flags >> 12) & 1;
-        const int k_per = st.k_blocks / t.z;  // K-blocks of this split-K slice
-        const int kb_begin = t.tz * k_per;
+        // K-blocks of this split-K slice, or of this balanced segment
+        const int k_per = bal ? (kbr & 0xffff) - (kbr >> 16) : st.k_blocks / t.z;
+        const int kb_begin = bal ? kbr >> 16 : t.tz * k_per;
         const int kb_end = kb_begin + k_per;
         // stage.wait() for reference k-step `ks` (policies.py:145-166)
         auto wait_kstep = [&](int ks) {
@@ -946,7 +1012,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
           // A split-K slice of a consumer still performs every k-step's wait of the
           // reference model (each z-slice of a tile runs all k-steps, engine.py:469-514):
           // the ones before its K range up front (they cover the k-step it starts in) ...
-          for (int ks = 0; ks * kbpk < kb_begin; ++ks) wait_kstep(ks);
+          // (a balanced segment waits only for what it reads: the k-step it starts inside;
+          // Row / Strided: k-step 0, the row's single wait)
+          int ks_lo = 0, ks_hi = (kb_begin + kbpk - 1) / kbpk;
+          if (bal) {
+            ks_lo = ordered ? kb_begin / kbpk : 0;
+            ks_hi = ordered ? ks_hi : (kb_begin > 0 ? 1 : 0);
+          }
+          for (int ks = ks_lo; ks < ks_hi; ++ks) wait_kstep(ks);
         }
         // conv K-block coordinates, advanced without divisions (rot = 0 for conv)
         int cv_sub = 0, cv_tap = 0, cv_ct = 0;
@@ -1049,7 +1122,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
           }
         }
         // ... and the ones after it once its loads are issued.
-        if (waits && rot == 0 && !(deep && !ordered))
+        if (waits && rot == 0 && !(deep && !ordered) && !bal)
           for (int ks = (kb_end + kbpk - 1) / kbpk; ks * kbpk < st.k_blocks; ++ks) wait_kstep(ks);
       }
     }
@@ -1065,12 +1138,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       uint32_t u = 0;  // TMEM accumulator-slot uses (a double-width tile takes two)
 #pragma unroll 1
       for (int it = 0;; ++it) {
-        const int g = ring_take(it, QD && !uleader);
+        int kbr;
+        const int g = ring_take(it, QD && !uleader, kbr);
         if (g < 0) break;
         const StageParams& sp = p.st[stage_of(p, g)];
         if (sp.kind == kStageDot || sp.kind == kStageAllReduce)
           continue;  // no MMA, no accumulator buffer
-        const int kblocks = sp.k_blocks / item_slices(sp, g - sp.item_begin);
+        const int kblocks = bal ? (kbr & 0xffff) - (kbr >> 16)
+                                : sp.k_blocks / item_slices(sp, g - sp.item_begin);
         const int wide = (C::kChunked && !QD) ? sp.wide : 0;
         // instruction descriptor: N = the stage's columns per MMA (chunked stages)
         const uint32_t idesc = C::kChunked ? ptx::idesc_f16(128 * CG, sp.half_n, AbFormat<T>::value)
@@ -1273,10 +1348,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
     uint32_t dmsg = 0, ddone = 0;  // dot_msg / dot_done phases (peer / leader)
 #pragma unroll 1
     for (int it = 0;; ++it) {
-      const int g = ring_take(it, CG == 2 && !uleader);
+      int kbr;
+      const int g = ring_take(it, CG == 2 && !uleader, kbr);
       if (g < 0) break;
       const Tile t = decode(p, g);
       const StageParams& st = p.st[t.s];
+      // balanced segment role (see Tile): 0 whole tile, 1 not the head, 2 head
+      const int brole = !bal ? 0
+                        : ((kbr >> 16) > 0 ? 1 : ((kbr & 0xffff) == st.k_blocks ? 0 : 2));
       if (st.kind == kStageAllReduce) {
         // Tensor-parallel all-reduce of one producer tile (extension): this
         // rank owns tiles lin = tb * world + rank. Wait for the tile's post on every rank
@@ -1455,7 +1534,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       // full-sector (32-B) stores when the output rows are 32-B aligned
       const bool v8ok = ((reinterpret_cast<uintptr_t>(st.c) | (st.ldc * sizeof(T))) & 31) == 0;
       constexpr int G = C::kEpiGroups;
-      if (C::kChunked && t.z == 2 && !((p.flags >> 29) & 1)) {
+      if (C::kChunked && !QD &&
+          (bal ? brole != 0 : (t.z == 2 && !((p.flags >> 29) & 1)))) {
         // Split-K slice (the reference's z > 1) of a CTA-pair tile, reduced into the
         // accumulator of the LAST slice to arrive (per tile half = per CTA): each slice
         // takes an arrival index from cnt[half]; the first z - 1 write their fp32 partial
@@ -1472,22 +1552,38 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         // on which slice arrives last (three or more would round differently run to run);
         // z > 2 takes the all-planes path below, which sums in slice order.
         // (diagnostic flag bit 29: the all-planes path for z = 2 as well)
-        const int tile_id = t.tx * st.grid_y + t.ty;
+        // Balanced (stream-K) segments use the same machinery with static roles: a
+        // segment that does not start its tile writes the plane of its unit and counts it
+        // into the tile half's ready counter; the head segment (K-block 0, the last item of
+        // its unit) waits for the ua..ub planes and reduces them into its accumulator.
+        const int tile_id = bal ? t.tb : t.tx * st.grid_y + t.ty;
         const int half_id = tile_id * CG * NP + static_cast<int>(qrank);
         int* cnt = st.cnt + half_id;
-        int* rdy = st.cnt + st.grid_x * st.grid_y * CG * NP + half_id;
+        int* rdy = bal ? cnt : st.cnt + st.grid_x * st.grid_y * CG * NP + half_id;
         const size_t plane = static_cast<size_t>(128) * acc_cols;
-        float* planes = st.ws + static_cast<size_t>(half_id) * t.z * plane;
+        // balanced head: the planes of units ua..ub (the ranges that start inside the tile)
+        const int bw = bal ? bal_width(st, units) : 1;
+        const int ua = bal ? (t.tb * st.k_blocks) / bw + 1 : 0;
+        float* planes = bal ? st.ws + (static_cast<size_t>(ua) * CG * NP + qrank) * plane
+                            : st.ws + static_cast<size_t>(half_id) * t.z * plane;
+        const size_t pstride = bal ? static_cast<size_t>(CG * NP) * plane : plane;
+        const int nparts = bal ? ((t.tb + 1) * st.k_blocks - 1) / bw - ua + 1 : t.z - 1;
         const int rl_row = ew * 32 + lane;
         const int row0 = t.tx * C::kTileM + static_cast<int>(rank) * 128;
         const int valid = st.m - row0 < 128 ? (st.m - row0 > 0 ? st.m - row0 : 0) : 128;
         const bool mine_ok = rl_row < valid;
         const int span = acc_cols / G;
-        if (threadIdx.x == 128) *split_flag = atomicAdd(cnt, 1);
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-        const int arrival = *split_flag;
-        if (arrival < t.z - 1) {
-          float* mine = planes + static_cast<size_t>(arrival) * plane;
+        int arrival;
+        if (bal) {
+          arrival = brole == 1 ? 0 : nparts;
+        } else {
+          if (threadIdx.x == 128) *split_flag = atomicAdd(cnt, 1);
+          asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+          arrival = *split_flag;
+        }
+        if (arrival < nparts) {
+          float* mine = bal ? st.ws + (static_cast<size_t>(unit) * CG * NP + qrank) * plane
+                            : planes + static_cast<size_t>(arrival) * plane;
 #pragma unroll 1
           for (int j = 0; j <= wide; ++j) {
             const int lo = max(eg * span, j * hn), hi = min((eg + 1) * span, (j + 1) * hn);
@@ -1514,7 +1610,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
           }
         } else {
           if (threadIdx.x == 128) {
-            sem_spin(p, rdy, t.z - 1);
+            sem_spin(p, rdy, nparts);
             *cnt = 0;  // every slice has arrived and every writer has counted: restore zero
             *rdy = 0;
           }
@@ -1544,12 +1640,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
                 for (int q = 0; q < 4; ++q) pa[c][q] = make_float4(0.f, 0.f, 0.f, 0.f);
               if (mine_ok) {
 #pragma unroll 1
-                for (int z = 0; z < t.z - 1; ++z) {
+                for (int z = 0; z < nparts; ++z) {
 #pragma unroll
                   for (int c = 0; c < kPC; ++c) {
                     if (x0 + 16 * c >= hi) break;
                     const float4* s4 = reinterpret_cast<const float4*>(
-                        planes + static_cast<size_t>(z) * plane +
+                        planes + static_cast<size_t>(z) * pstride +
                         (static_cast<size_t>((x0 + 16 * c) / 16) * 512 + rl_row) * 4);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
@@ -1827,7 +1923,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
           if constexpr (CG == 2)
             ptx::mbar_wait_cluster(&peer_done[local % kPeerRing], (local / kPeerRing) & 1);
           const uint64_t tnow = ptx::global_timer();
-          if (st.n_out_deps > 0) {
+          // a balanced segment that does not start its tile only contributed a partial:
+          // the tile is posted once, by its head segment after the reduction
+          const bool posts = brole != 1;
+          if (st.n_out_deps > 0 && posts) {
             // release: the epilogue's stores (ordered before this thread by the named
             // barrier) become visible before the post; diagnostic flag bit 22 times the
             // post without the full fence
@@ -1880,7 +1979,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
               }
             }
           }
-          if (st.out_sem != nullptr) {
+          if (st.out_sem != nullptr && posts) {
             // the tile's rows (both CTAs of a pair) are stored: let a copy stream read
             // them (a PCIe agent, hence system scope)
             __threadfence_system();

@@ -155,6 +155,9 @@ class CuSync:
     wait_kernel: str = "auto"
     adversarial: bool = False
     coresident_grid: tuple | None = None  # CTAs (pairs) per stage launch; None = per tile
+    # static stream-K schedule (TS_FLAG_BALANCED): every CTA pair runs an equal K-block
+    # range of each GeMM stage, tiles split across pairs are reduced by their head segment
+    balanced: bool = False
     device: torch.device | None = None
     stages: list[CuStage] = field(default_factory=list)
     deps: list[CuDep] = field(default_factory=list)
@@ -468,6 +471,9 @@ class CuSync:
                    | self.extra_flags)
         d.num_ctas = self.num_ctas
         d.cluster_pairs = self.cluster_pairs
+        if self.balanced:
+            d.flags |= _lib.TS_FLAG_BALANCED
+            self._balanced_buffers(d)
         if self._scratch is None:
             self._scratch = torch.zeros(_lib.TS_SCRATCH_INTS, dtype=torch.int32,
                                         device=self.device)
@@ -479,6 +485,40 @@ class CuSync:
                 raise ConfigError("the all-reduce stage needs set_peers(...) before launch")
             d.peers = ctypes.pointer(self._peers)
         return d
+
+    def balanced_units(self) -> int:
+        """Work units (CTA pairs) of a balanced launch: one per SM pair, capped at the
+        co-resident cluster count (ts_chain_units), or num_ctas / 2."""
+        out = ctypes.c_int()
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().ts_chain_units(self.tile_n, self.cta_group, 1, 0,
+                                                  _DT[self.stages[0].a.dtype],
+                                                  ctypes.byref(out)))
+        units = out.value
+        if self.num_ctas:
+            units = min(units, self.num_ctas // self.cta_group)
+        return units
+
+    def _balanced_buffers(self, d) -> None:
+        """Per stage: fp32 partial planes [units][2 CTAs][128 rows][tile width] (one per
+        unit: only a unit's first segment of a stage can start inside a tile) and one
+        ready counter per tile half (zero; the head segment restores it)."""
+        if self.mode != "fused" or self.cta_group != 2 or self.tile_n != 256 or self.swap_ab \
+                or self.cluster_pairs != 1:
+            raise ConfigError("balanced=True needs mode='fused', cta_group=2, tile_n=256, "
+                              "cluster_pairs=1")
+        units = self.balanced_units()
+        for i, st in enumerate(self.stages):
+            if st.kind != "gemm" or st.splits != 1 or st.tail[0] or st.epilogue == "swiglu":
+                raise ConfigError(f"stage {st.id}: the balanced schedule takes unsplit GeMM "
+                                  "stages (no tail, no SwiGLU)")
+            need = units * 2 * BM * st.width
+            if st.ws is None or st.ws.numel() < need:
+                st.ws = torch.empty(need, dtype=torch.float32, device=st.a.device)
+                st.cnt = torch.zeros(2 * st.grid.x * st.grid.y, dtype=torch.int32,
+                                     device=st.a.device)
+            d.stages[i].workspace = st.ws.data_ptr()
+            d.stages[i].counters = st.cnt.data_ptr()
 
     def enable_trace(self, capacity: int | None = None) -> None:
         """Record the reference's per-block events on the device (engine.py:220-248)."""
