@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--fused-allreduce", action="store_true",
+                    help="also time the chain with the tensor-parallel all-reduce fused into "
+                         "it (FusedTPMlp over torch symmetric memory) beside chain + NCCL")
     ap.add_argument("--plan", choices=["auto", "fixed"], default="auto",
                     help="auto: time the planner's candidates; fixed: the B=1024 headline "
                          "configuration without the search (for profiling runs)")
@@ -87,7 +90,7 @@ class ClockSampler:
                 self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.0005)  # the timed region can be a few ms (20 chains)
 
     def __enter__(self):
         if self.ok:
@@ -283,6 +286,23 @@ def main():
         record_kernel[0] = False
     us_stream = time_steps(step_stream, args.steps, args.warmup, torch, dist if use_dist else None)
     us_cublas = time_steps(step_cublas, args.steps, args.warmup, torch, dist if use_dist else None)
+    us_fused_ar = None
+    if args.fused_allreduce:
+        # the all-reduce inside the chain: tile t summed by rank t % world over NVLink peer
+        # memory as soon as every rank posted it (tp.FusedTPMlp, symmetric-memory pointers)
+        from paper_2305_13450_b200.tp import FusedTPMlp
+        if not use_dist:
+            import socket
+            so = socket.socket()
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+            so.close()
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev,
+                                    init_method=f"tcp://127.0.0.1:{port}")
+        # (a stage that feeds the all-reduce cannot carry last-wave tail slices)
+        far = FusedTPMlp.from_group(x, w1, w2, **dict(best, cons_tail=(0, 1)))
+        us_fused_ar = time_steps(far, args.steps, args.warmup, torch, dist if use_dist else None)
+        assert not far.chain.cs.watchdog_fired(), "semaphore watchdog fired (fused all-reduce)"
 
     # kernel-only duration of the chain launch (roofline denominator): the average of the
     # per-launch CUDA-event durations recorded inside the timed region, on the launch stream
@@ -332,7 +352,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_sweep:
         sweep = {"gpt3_mlp": planner.sweep_mlp(batches=(1, 64, 256, 512, 1024, 2048), device=dev),
                  "gpt3_attention": planner.sweep_attention(device=dev),
-                 "resnet38_conv_pairs": planner.sweep_conv(batches=(1, 8, 32), device=dev),
+                 "resnet38_conv_pairs": planner.sweep_conv(batches=(1, 8, 32, 128, 256),
+                                                           device=dev),
+                 "vgg19_conv_pairs": planner.sweep_conv(batches=(1, 8, 32),
+                                                        layers=planner.VGG19_LAYERS, device=dev),
                  "llama8b_swiglu": planner.sweep_swiglu(device=dev)}
 
     if rank != 0:
@@ -375,6 +398,7 @@ def main():
                    "chain": chain_s, "l2": "inputs larger than L2 (weights 302 MB)"},
         "stream_sync_us": round(us_stream, 2), "speedup_vs_stream": round(us_stream / us, 4),
         "cublas_us": round(us_cublas, 2), "speedup_vs_cublas": round(us_cublas / us, 4),
+        **({"fused_allreduce_us": round(us_fused_ar, 2)} if us_fused_ar is not None else {}),
         "kernel_us": round(us_kernel, 2),
         "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": burst,
                      "unit": "TFLOP/s", "frac": round(achieved / burst, 4), "traffic": traffic,
@@ -385,7 +409,7 @@ def main():
         "gpu_launches": args.steps,
         "clocks": sampler.summary(),
     }
-    if use_dist:
+    if dist.is_initialized():
         dist.destroy_process_group()
     sys.stdout.flush()
     print(json.dumps(out), flush=True)

@@ -1535,7 +1535,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       const bool v8ok = ((reinterpret_cast<uintptr_t>(st.c) | (st.ldc * sizeof(T))) & 31) == 0;
       constexpr int G = C::kEpiGroups;
       if (C::kChunked && !QD &&
-          (bal ? brole != 0 : (t.z == 2 && !((p.flags >> 29) & 1)))) {
+          (bal ? brole != 0 : (t.z >= 2 && t.z <= 4 && !((p.flags >> 29) & 1)))) {
         // Split-K slice (the reference's z > 1) of a CTA-pair tile, reduced into the
         // accumulator of the LAST slice to arrive (per tile half = per CTA): each slice
         // takes an arrival index from cnt[half]; the first z - 1 write their fp32 partial
@@ -1548,10 +1548,13 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         // the last slice's own partial never leaves TMEM. Every slice still posts once
         // below (consumers wait for expected x z; each post follows its own slice's work,
         // and the count completes only after the reducing slice has stored).
-        // Two slices only: a + b is exact in either order, so the result does not depend
-        // on which slice arrives last (three or more would round differently run to run);
-        // z > 2 takes the all-planes path below, which sums in slice order.
-        // (diagnostic flag bit 29: the all-planes path for z = 2 as well)
+        // Two slices: a + b is exact in either order, so the result does not depend on
+        // which slice arrives last. Three or four: a reduction order that depends on the
+        // arrival order would round differently run to run, so the owner is static — the
+        // last slice in claim order (claimed last, it finishes last in the common case)
+        // sums planes 0 .. z-2 in slice order into its accumulator; slices 0 .. z-2
+        // write their planes and never wait. z > 4 takes the all-planes path below.
+        // (diagnostic flag bit 29: the all-planes path for z = 2..4 as well)
         // Balanced (stream-K) segments use the same machinery with static roles: a
         // segment that does not start its tile writes the plane of its unit and counts it
         // into the tile half's ready counter; the head segment (K-block 0, the last item of
@@ -1576,6 +1579,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         int arrival;
         if (bal) {
           arrival = brole == 1 ? 0 : nparts;
+        } else if (t.z > 2) {
+          arrival = t.tz == t.z - 1 ? nparts : t.tz;  // static owner: the last slice
         } else {
           if (threadIdx.x == 128) *split_flag = atomicAdd(cnt, 1);
           asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");

@@ -102,12 +102,17 @@ def candidates(m: int, mode: str, n2: int | None = None, units: int = 74,
                                 prod_tile_n=512, cons_tile_n=512, prod_splits=z1))
             if n2 and n2 % 512 == 0:
                 # last-wave balancing: GeMM2's final partial wave as split-K slices
-                rem = (-(-m // 256) * (n2 // 512)) % units
+                tiles2 = -(-m // 256) * (n2 // 512)
+                rem = tiles2 % units
                 if rem:
-                    for co, z1, zt in itertools.product(orders, (1, 2), (2, 3)):
+                    # GeMM1 in 3 slices finishes in ~2 waves of short items (B=1024: 144 on
+                    # 74 pairs) instead of a full second wave gating its last row; the tail
+                    # sizes bracket GeMM2's partial last wave
+                    tails = sorted({rem, min(tiles2, rem + units // 2)})
+                    for co, z1, zt, tt in itertools.product(orders, (1, 2, 3), (2, 3), tails):
                         out.append(dict(policy=RowSync(), mode=mode, tile_n=tn, cta_group=cg,
                                         cons_order=co, prod_tile_n=512, cons_tile_n=512,
-                                        prod_splits=z1, cons_tail=(rem, zt)))
+                                        prod_splits=z1, cons_tail=(tt, zt)))
         if (cg, tn) == (2, 256) and m >= 256:
             # two-pair clusters: the 256 x 512 tile on two CTA pairs sharing the activation
             # rows by multicast (24 KB of operands per SM and K-block, double-buffered
@@ -249,6 +254,10 @@ def wave_table(m: int, n1: int, n2: int, tile_m: int, tile_n: int, sms: int = 14
 
 
 RESNET38_LAYERS = ((56, 64), (28, 128), (14, 256), (7, 512))
+# VGG-19's 3x3 "same" conv pairs with equal in/out channels, one per resolution stage
+# (Simonyan & Zisserman 2015, config E: 2x64 @224, 2x128 @112, 4x256 @56, 4x512 @28,
+# 4x512 @14); BASELINE.json configs[4] names VGG-19 beside ResNet-38 (no reference text)
+VGG19_LAYERS = ((224, 64), (112, 128), (56, 256), (28, 512), (14, 512))
 
 
 def conv_candidates(c: int, mode: str, m: int = 1 << 30):

@@ -156,9 +156,10 @@ class FusedTPMlp:
     NCCL call. Tile ownership is round-robin (tile t belongs to rank t % world).
 
     Peers are connected with ``connect_group`` (one process addressing every member's
-    memory: a single GPU simulating the group, or one process driving P2P-enabled GPUs);
-    a multi-process group passes IPC-mapped / symmetric-memory pointers to
-    ``cs.set_peers`` (``handles`` lists what each rank must publish).
+    memory: a single GPU simulating the group, or one process driving P2P-enabled GPUs),
+    or — one process per GPU — with ``FusedTPMlp.from_group``, which allocates the
+    exchanged buffers in torch symmetric memory and rendezvouses them over the process
+    group (``handles`` lists what each rank publishes).
     """
 
     def __init__(self, x: torch.Tensor, w1_shard: torch.Tensor, w2_shard: torch.Tensor,
@@ -178,6 +179,49 @@ class FusedTPMlp:
 
     def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         return self.chain(stream)
+
+    @classmethod
+    def from_group(cls, x: torch.Tensor, w1_shard: torch.Tensor, w2_shard: torch.Tensor,
+                   group=None, policy: SyncPolicy = RowSync(), **chain_kw) -> "FusedTPMlp":
+        """One rank of a multi-process tensor-parallel group (one process per GPU, the
+        group initialised with torch.distributed): the all-reduced output Y, the
+        GeMM2 -> all-reduce semaphores and the done counter are allocated in torch's
+        symmetric memory and exchanged with ``rendezvous`` (CUDA IPC / cuMem handles over
+        the group's store), so every rank's kernel addresses its peers' buffers directly
+        over NVLink — the pointer exchange ``connect_group`` does within one process.
+        Collective: every rank of `group` must call it with the same shapes."""
+        import torch.distributed._symmetric_memory as symm
+        self = cls(x, w1_shard, w2_shard, policy=policy, **chain_kw)
+        cs = self.chain.cs
+        dev = x.device
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        y = symm.empty(*self.chain.y.shape, dtype=x.dtype, device=dev)
+        dep = cs.allreduce_dep()
+        sem = symm.empty(dep.sem.numel(), dtype=torch.int32, device=dev)
+        done = symm.empty(1, dtype=torch.int32, device=dev)
+        sem.zero_()
+        done.zero_()
+        # the consumer GeMM writes Y and the all-reduce stage sums it in place
+        self.chain.y = y
+        self.chain.cons.c = y
+        for st in cs.stages:
+            if st.kind == "allreduce":
+                st.a = st.b = st.c = y
+        dep.sem = sem
+        cs._ar_done = done
+        handles = [symm.rendezvous(t, group if group is not None else dist.group.WORLD)
+                   for t in (y, sem, done)]
+        torch.cuda.synchronize(dev)
+        # a tensor may sit at an offset inside its symmetric allocation: same offset on
+        # every rank (collective allocation of equal shapes)
+        bufs, sems, dones = ([int(p) + t.data_ptr() - int(h.buffer_ptrs[rank])
+                              for p in h.buffer_ptrs]
+                             for h, t in zip(handles, (y, sem, done)))
+        cs.set_peers(rank, bufs, sems, dones)
+        self._symm = handles  # keep the mappings alive
+        if world > 1:
+            dist.barrier(group)
+        return self
 
 
 def connect_group(members: list[FusedTPMlp]) -> None:

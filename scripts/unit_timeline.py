@@ -23,18 +23,25 @@ def main(path, show=4):
     stats = defaultdict(float)
     makespan = (recs[-1][0] - t0) / 1e3
     for sm, rs in by_sm.items():
-        cur = None
-        lst = []
+        # each role (scheduler, MMA warp, epilogue) handles a unit's items in claim order,
+        # so the i-th record of a once-per-item kind belongs to the unit's i-th item
+        seq = defaultdict(list)
         for r in rs:
-            t = (r[0] - t0) / 1e3
-            k = KIND.get(r[1], str(r[1]))
-            if k == "sched":
-                cur = {"stage": d["stages"][r[2]], "tb": r[3], "sched": t}
-                lst.append(cur)
-            elif cur is not None and k in ("mma_b", "mma_e", "epi_b", "epi_e", "fin", "part",
-                                           "wait_b", "wait_e"):
-                # MMA / epilogue records of the current item (in-order per unit)
-                cur.setdefault(k, t)
+            seq[KIND.get(r[1], str(r[1]))].append(r)
+        lst = []
+        for i, r in enumerate(seq["sched"]):
+            it = {"stage": d["stages"][r[2]], "tb": r[3], "sched": (r[0] - t0) / 1e3}
+            for k in ("mma_b", "mma_e", "epi_b", "epi_e", "fin"):
+                if i < len(seq[k]):
+                    it[k] = (seq[k][i][0] - t0) / 1e3
+            lst.append(it)
+        # waits and partial-plane records carry their item's (stage, tb)
+        for k in ("wait_b", "wait_e", "part"):
+            for r in seq[k]:
+                for it in lst:
+                    if it["stage"] == d["stages"][r[2]] and it["tb"] == r[3] and k not in it:
+                        it[k] = (r[0] - t0) / 1e3
+                        break
         items[sm] = lst
     units = sorted(items)
     mma_busy, first_mma, last_end = [], [], []

@@ -120,14 +120,18 @@ def main() -> None:
             add(f"llama_swiglu_tp{tp}_b{b}", [("gate_up", g1, 4096 // (pw // 2), rm),
                                              ("down", g2, f // (pw // 2), rm)],
                 [("gate_up", "down", "a", (p, 0))])
-    # ResNet-38 conv pairs (Conv2DTileSync(9)): the sweep's configurations
-    for (hw, c), b in itertools.product(planner.RESNET38_LAYERS, (1, 8, 32, 128, 256)):
+    # ResNet-38 / VGG-19 conv pairs (Conv2DTileSync(9)): the sweeps' configurations
+    conv_cases = [("resnet38", L, b) for L, b in
+                  itertools.product(planner.RESNET38_LAYERS, (1, 8, 32, 128, 256))]
+    conv_cases += [("vgg19", L, b) for L, b in
+                   itertools.product(planner.VGG19_LAYERS, (1, 8, 32))]
+    for net, (hw, c), b in conv_cases:
         for kw in planner.conv_candidates(c, "fused", b * hw * hw):
             tm = 128 * kw["cta_group"]
             gx = -(-(b * hw * hw) // tm)
             z = kw["prod_splits"]
             g = (gx, c // kw["tile_n"], z)
-            add(f"resnet38_conv_{hw}x{c}_b{b}", [("conv1", g, 9 * c // kw["tile_n"], rm),
+            add(f"{net}_conv_{hw}x{c}_b{b}", [("conv1", g, 9 * c // kw["tile_n"], rm),
                                                 ("conv2", g, 9 * (c // kw["tile_n"]), rm)],
                 [("conv1", "conv2", "a", ("conv2d", 9))])
     (OUT / "bench_scenarios.json").write_text(json.dumps(recs, separators=(",", ":")))

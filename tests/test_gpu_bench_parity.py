@@ -200,3 +200,24 @@ def test_resnet38_conv_pair_b32(hw, c):
         torch.cuda.synchronize()
         check_sync(ch.cs)
         check_close(ch.y, y_ref, torch.float16)
+
+
+@pytest.mark.parametrize("hw,c", planner.VGG19_LAYERS)
+def test_vgg19_conv_pair(hw, c):
+    """VGG-19 3x3 conv pairs (BASELINE.json configs[4]) at batch 1, Conv2DTileSync(9), the
+    configurations the bench's VGG sweep times (the first two candidates per mode)."""
+    g = torch.Generator().manual_seed(hw + c)
+    x = torch.randn(1, hw, hw, c, generator=g).half()
+    w1 = (torch.randn(c, 3, 3, c, generator=g) / (9 * c) ** 0.5).half()
+    w2 = (torch.randn(c, 3, 3, c, generator=g) / (9 * c) ** 0.5).half()
+    _, y_ref = O.conv_chain(x.float().numpy(), w1.float().numpy(), w2.float().numpy(), "fp16")
+    xd, w1d, w2d = x.cuda(), w1.cuda(), w2.cuda()
+    for mode in ("fused", "stream"):
+        for kw in planner.conv_candidates(c, mode, hw * hw)[:2]:
+            ch = ts.ConvChain(xd, w1d, w2d, keep_sems=True, **kw)
+            ch()
+            torch.cuda.synchronize()
+            assert not ch.cs.watchdog_fired()
+            check_close(ch.y, y_ref, torch.float16)
+            if mode == "fused":
+                check_sync(ch.cs)
