@@ -84,7 +84,10 @@ def candidates(m: int, mode: str, n2: int | None = None, units: int = 74,
         orders = [RowMajor()] + ([BandedColumnMajor(min(gx, 4))] if gx > 1 else [])
         # per-stage widths: CTA-pair 256-wide chains may give either stage double-width
         # (256 x 512) tiles — fewer operand bytes per MAC, coarser wave quantization
-        widths = [(0, 0), (0, 512), (512, 512), (512, 0)] if (cg, tn) == (2, 256) else [(0, 0)]
+        # (256 x 384 = two N = 192 MMAs: B=1024's GeMM1 as 64 tiles keeps 64 of 74 pairs
+        # busy instead of 48)
+        widths = ([(0, 0), (0, 512), (512, 512), (512, 0), (384, 512), (384, 384)]
+                  if (cg, tn) == (2, 256) else [(0, 0)])
         for pol, co, (pw, cw) in itertools.product(pols, orders, widths):
             out.append(dict(policy=pol, mode=mode, tile_n=tn, cta_group=cg, cons_order=co,
                             prod_tile_n=pw, cons_tile_n=cw))
@@ -113,6 +116,10 @@ def candidates(m: int, mode: str, n2: int | None = None, units: int = 74,
                         out.append(dict(policy=RowSync(), mode=mode, tile_n=tn, cta_group=cg,
                                         cons_order=co, prod_tile_n=512, cons_tile_n=512,
                                         prod_splits=z1, cons_tail=(tt, zt)))
+                    for co, zt in itertools.product(orders, (2, 3)):
+                        out.append(dict(policy=RowSync(), mode=mode, tile_n=tn, cta_group=cg,
+                                        cons_order=co, prod_tile_n=384, cons_tile_n=512,
+                                        cons_tail=(rem, zt)))
         if (cg, tn) == (2, 256) and m >= 256:
             # two-pair clusters: the 256 x 512 tile on two CTA pairs sharing the activation
             # rows by multicast (24 KB of operands per SM and K-block, double-buffered

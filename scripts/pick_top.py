@@ -14,5 +14,5 @@ for b in [int(a) for a in sys.argv[1:]] or [1024]:
     w2 = (torch.randn(H, FFN, device="cuda") / FFN ** 0.5).half()
     best, cands = planner.pick_mlp(x, w1, w2, mode="fused")
     print(f"B={b}: pick {planner.describe(best)}")
-    for d, us in sorted(cands, key=lambda c: c[1])[:12]:
-        print(f"   {us:7.1f} us  {d}")
+    for d in sorted(cands, key=lambda c: c["us"])[:12]:
+        print(f"   {d['us']:7.1f} us  " + str({k: v for k, v in d.items() if k != 'us'}))
