@@ -83,13 +83,16 @@ class ClockSampler:
         except Exception:
             self.max = None
 
+    def _sample(self):
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            pass
+
     def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-            except Exception:
-                pass
+            self._sample()
             time.sleep(0.0005)  # the timed region can be a few ms (20 chains)
 
     def __enter__(self):
@@ -101,6 +104,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.ok:
+            self._sample()  # the end of the timed region (the GPU just went idle)
             self._stop.set()
             self._t.join()
 
@@ -112,7 +116,7 @@ class ClockSampler:
                 "reasons": names, "samples": len(self.samples)}
 
 
-def time_steps(fn, steps, warmup, torch, dist=None):
+def time_steps(fn, steps, warmup, torch, dist=None, poll=None):
     """Device time per step (us): W untimed steps, then exactly K steps bracketed by a
     barrier and synchronize, timed with CUDA events on the launching stream; max over
     ranks."""
@@ -128,6 +132,12 @@ def time_steps(fn, steps, warmup, torch, dist=None):
     for _ in range(steps):
         fn()
     e1.record(s)
+    if poll is not None:
+        # clock samples while the enqueued steps run (the launches return at once, so the
+        # timed region on the device is mostly ahead of the host here)
+        while not e1.query():
+            poll()
+            time.sleep(0.0002)
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / steps
     if dist is not None:
@@ -282,7 +292,8 @@ def main():
     torch.cuda.synchronize()
     with sampler:
         record_kernel[0] = True
-        us = time_steps(step, args.steps, 0, torch, dist if use_dist else None)
+        us = time_steps(step, args.steps, 0, torch, dist if use_dist else None,
+                        poll=sampler._sample if sampler.ok else None)
         record_kernel[0] = False
     us_stream = time_steps(step_stream, args.steps, args.warmup, torch, dist if use_dist else None)
     us_cublas = time_steps(step_cublas, args.steps, args.warmup, torch, dist if use_dist else None)
