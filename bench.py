@@ -397,7 +397,8 @@ def main():
     d = planner.describe(best)
     chain_s = (f"{d['mode']} {d['policy']} {d['tile']} cg{d['cta_group']} "
                f"splits{d['splits'][0]}/{d['splits'][1]} {d['consumer_order']}"
-               + (f" tail{d['consumer_tail']}" if "consumer_tail" in d else ""))
+               + (f" tail{d['consumer_tail']}" if "consumer_tail" in d else "")
+               + (f" reduce:{d['reduce']}" if "reduce" in d else ""))
     out = {
         "metric": "GPT-3 MLP/attn dependent-GeMM latency (µs), speedup vs stream-sync baseline",
         "value": round(us, 2), "unit": "us", "n_gpus": world, "steps": args.steps,

@@ -126,6 +126,31 @@ int make_tmap(CUtensorMap* m, const void* ptr, int rows, int k, int ld, int dtyp
   return TS_OK;
 }
 
+// Split-K partial planes of a CTA-pair 256-wide stage: the fp32 workspace viewed as
+// [rows][cols] (rows = planes x 128), 32-column x 128-row boxes with 128-B swizzle — the A
+// operand of the owner slice's reduction MMAs (kind::tf32).
+int make_tmap_ws(CUtensorMap* m, const float* ptr, long long rows, int cols) {
+  const TmapKey key{ptr, {2, rows, cols, 0, 0, 0}};
+  if (const CUtensorMap* hit = g_tmaps.find(key)) {
+    *m = *hit;
+    return TS_OK;
+  }
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(TS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 4};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TS_ERR_CUDA, "cuTensorMapEncodeTiled (workspace) failed (%d) rows=%lld cols=%d",
+                (int)r, rows, cols);
+  g_tmaps.put(key, *m);
+  return TS_OK;
+}
+
 using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                     const cuuint64_t*, const cuuint64_t*, const int*,
                                     const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
@@ -534,6 +559,18 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       if (np == 2) {  // 64-row activation boxes: each CTA multicasts half of its rows
         r = make_tmap(&sp.tmap_a_half, st.a, st.m, st.k, st.lda, st.dtype, 64);
         if (r) return r;
+      }
+      // split-K / tail slices of a CTA-pair 256-wide stage: the owner slice streams the
+      // other slices' planes in by TMA (workspace: tiles x slices x 256 rows x tile width)
+      const int zmax = sp.tail_tiles > 0 ? sp.tail_splits : sp.splits;
+      // (flag bit 27: measured per plan — faster for some B=1024 plans, slower than the
+      // register reductions at B=256/512 — so the planner tries it as a candidate)
+      if (((d->flags >> 27) & 1) && cg == 2 && bn == 256 && !swap && np == 1 && !conv &&
+          zmax > 1 && st.workspace != nullptr && sp.kind == ts::kStageGemm) {
+        const long long rows = static_cast<long long>(sp.grid_x) * sp.grid_y * zmax * 256;
+        r = make_tmap_ws(&sp.tmap_ws, st.workspace, rows, half_n << wide);
+        if (r) return r;
+        sp.red_mma = 1;
       }
     }
   }

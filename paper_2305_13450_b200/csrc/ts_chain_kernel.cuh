@@ -72,6 +72,10 @@ struct StageParams {
   CUtensorMap tmap_a;  // activations [m, k] K-major, 128-B swizzle
   CUtensorMap tmap_b;  // weights [n, k] K-major, 128-B swizzle
   CUtensorMap tmap_a_half;  // two-pair clusters: activations, 64-row boxes (multicast halves)
+  // split-K partial planes (chunked CTA-pair tiles): ws as fp32 [planes x 128 rows][tile
+  // columns], 32-column x 128-row boxes, 128-B swizzle — the A operand of the reduction MMAs
+  CUtensorMap tmap_ws;
+  int red_mma;  // 1: tmap_ws is valid and split-K owners reduce on the tensor cores
   void* c;
   int m, n, k, ldc;
   int grid_x, grid_y;
@@ -173,7 +177,7 @@ struct Cfg {
   // 256 x 256 tiles at 4 K-blocks = 2048 MMA cycles of buffering, too little to cover
   // loaded HBM latency: 31-51% of the MMA floor against cuBLAS's 97% on the same tile.)
 #ifndef TS_CHUNKS
-#define TS_CHUNKS 12
+#define TS_CHUNKS 11
 #endif
   static constexpr int kChunks = TS_CHUNKS;
   static constexpr int kTileM = SW ? BN : 128 * CG;  // activation rows of a tile
@@ -199,8 +203,10 @@ struct Cfg {
 #ifndef TS_STAGE_WARP_BYTES
 #define TS_STAGE_WARP_BYTES 4096
 #endif
-  static constexpr int kBarOffset =
-      kChunked ? kStageOff + (kEpiThreads / 32) * TS_STAGE_WARP_BYTES : kStages * kStageBytes;
+  // chunked tiles: a 4-KB tf32 identity (the B operand of the split-K reduction MMAs,
+  // 32 x 32 for one CTA, this CTA's 16 rows of it for a pair) after the staging blocks
+  static constexpr int kIdentOff = kStageOff + (kEpiThreads / 32) * TS_STAGE_WARP_BYTES;
+  static constexpr int kBarOffset = kChunked ? kIdentOff + 4096 : kStages * kStageBytes;
   // K-block full, commit-group empty; tmem full/empty x2; tile ring full/empty; peer_done
   static constexpr int kNumBars = kFullRing + kCommitRing + 4 + 2 * kTileRing + kPeerRing + 2;
   // + tile ring ids, TMEM slot, flags and the last-arriver dot list (64 ints), ring-entry
@@ -645,6 +651,51 @@ __device__ __forceinline__ void allreduce_rows(const ChainParams& p, const Stage
 // next (a 256 x 512 tile on one pair fills all of TMEM). Ring entries are freed by both
 // pairs' MMA commits (empty barriers count 2); the cluster leader claims items, hands the
 // id to the other three CTAs and posts once all four have stored.
+// Split-K owner, producer side: wait until the other slices' fp32 partial planes of this
+// CTA's rows are written, then stream them in as 32-column x 128-row boxes (the A operand
+// of the tensor-core reduction D += P x I), one ring chunk and one commit group per box.
+// Out of line: the scheduler lane is the kernel's tightest register budget.
+template <int CG, typename C>
+__device__ __noinline__ void owner_plane_loads(const ChainParams& p, const StageParams& st,
+                                               const Tile& t, int rank, bool leader,
+                                               uint32_t plead, int acc_cols, uint8_t* smem,
+                                               uint64_t* full, uint64_t* empty, int* owner,
+                                               int& ea, uint32_t& kq, uint32_t& cid,
+                                               uint64_t pol) {
+  constexpr int R = C::kRing;
+  const int half_id = (t.tx * st.grid_y + t.ty) * CG + rank;
+  int* rdy = st.cnt + st.grid_x * st.grid_y * CG + half_id;
+  sem_spin(p, rdy, t.z - 1);
+  *rdy = 0;  // every writer has counted: restore the zero invariant
+  ptx::fence_proxy_async_global();
+  const int groups = acc_cols / 32;
+#pragma unroll 1
+  for (int pz = 0; pz < t.z - 1; ++pz) {
+#pragma unroll 1
+    for (int j = 0; j < groups; ++j) {
+      const int e = ea;
+      const int o = owner[e];
+      if (o >= 0) {
+        const uint32_t uo = static_cast<uint32_t>(o);
+        ptx::mbar_wait(&empty[uo % kCommitRing], (uo / kCommitRing) & 1);
+      }
+      owner[e] = static_cast<int>(cid);
+      ea = wrap_inc(ea, R);
+      uint64_t* fb = &full[kq % kFullRing];
+      if (leader) ptx::mbar_arrive_expect_tx(fb, CG * C::kChunkBytes);
+      const int prow = (half_id * t.z + pz) * 128;
+      if constexpr (CG == 2) {
+        ptx::tma_load_2d_pair(smem + e * C::kChunkBytes, &st.tmap_ws, ptx::mapa(fb, plead),
+                              j * 32, prow, pol);
+      } else {
+        ptx::tma_load_2d(smem + e * C::kChunkBytes, &st.tmap_ws, fb, j * 32, prow, pol);
+      }
+      ++kq;
+      ++cid;
+    }
+  }
+}
+
 template <int BN, int CG, typename T, bool SW, bool QD = false>
 __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
     chain_kernel(const __grid_constant__ ChainParams p) {
@@ -714,6 +765,18 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
     }
     *dot_count = 0;
     ptx::fence_barrier_init();
+  }
+  if constexpr (C::kChunked && !QD) {
+    // tf32 identity rows of this CTA (K-major, 128-B swizzle: element (n, k) of an 8-row
+    // group at n * 128 + ((k / 4) ^ (n & 7)) * 16 + (k % 4) * 4); a CTA pair's B operand
+    // of N = 32 is split by rows: rank r holds rows [16 r, 16 r + 16)
+    float* id = reinterpret_cast<float*>(smem + C::kIdentOff);
+    for (int i = threadIdx.x; i < 1024; i += C::kThreads) {
+      const int n = i >> 5, k = i & 31;
+      const int ng = (CG == 2 ? 16 * static_cast<int>(rank) : 0) + n;  // global N row
+      id[(n * 128 + (((k >> 2) ^ (n & 7)) << 4) + ((k & 3) << 2)) >> 2] = (k == ng) ? 1.f : 0.f;
+    }
+    ptx::fence_proxy_async_shared();
   }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.n_stages; ++s) {
@@ -1124,6 +1187,17 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         // ... and the ones after it once its loads are issued.
         if (waits && rot == 0 && !(deep && !ordered) && !bal)
           for (int ks = (kb_end + kbpk - 1) / kbpk; ks * kbpk < st.k_blocks; ++ks) wait_kstep(ks);
+        if constexpr (C::kChunked && !QD) {
+          // Split-K owner (the last slice of a CTA-pair tile): once the other slices' fp32
+          // partial planes of this CTA's rows are written, stream them in as 32-column x
+          // 128-row boxes — the A operand of the tensor-core reduction D += P x I (see the
+          // MMA warp) — so the sum is TMA-fed and bandwidth-bound instead of a register
+          // loop at loaded-L2 latency. One ring chunk and one commit per box.
+          if (st.red_mma && !bal && t.z >= 2 && t.tz == t.z - 1 && !((p.flags >> 29) & 1)) {
+            owner_plane_loads<CG, C>(p, st, t, static_cast<int>(rank), leader, plead, hn << wide,
+                                     smem, full, empty, owner, ea, kq, cid, pol_first);
+          }
+        }
       }
     }
   } else if (warp == 1) {
@@ -1237,6 +1311,43 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
           }
           ++kq;
           __syncwarp();
+        }
+        if constexpr (C::kChunked && !QD) {
+          // split-K owner: D[:, 32 j .. 32 j + 32) += P_z[:, 32 j ..] x I for every other
+          // slice's plane P_z (kind::tf32: the partial enters the fp32 accumulator at tf32
+          // precision, 2^-11 relative — below the fp16/bf16 output rounding), one ring
+          // chunk per 32-column box, committed box by box like a K-block
+          if (!bal) {
+            const Tile tt = decode(p, g);
+            if (sp.red_mma && tt.z >= 2 && tt.tz == tt.z - 1 && !((p.flags >> 29) & 1)) {
+              const int hn = sp.half_n;
+              const int groups = (hn << wide) / 32;
+              const uint32_t idesc_r = ptx::idesc_tf32(128 * CG, 32);
+              const uint64_t bd = ptx::smem_desc_k_sw128(ptx::smem_u32(smem + C::kIdentOff));
+#pragma unroll 1
+              for (int rb = 0; rb < (tt.z - 1) * groups; ++rb) {
+                const int col = (rb % groups) * 32;
+                ptx::mbar_wait(&full[kq % kFullRing], (kq / kFullRing) & 1);
+                ptx::tc_fence_after();
+                if (lane == 0) {
+                  const uint32_t dcol = tmem_base + ((u + col / hn) & 1) * C::kAccCols + (col % hn);
+                  if (!no_mma && !((p.flags >> 30) & 1))  // bit 30: diagnostic, no reduction MMAs
+                    ptx::umma_tf32_kblock<CG>(dcol, ptx::smem_desc_k_sw128(
+                                                        ptx::smem_u32(smem + ea * C::kChunkBytes)),
+                                              bd, idesc_r);
+                  if constexpr (CG == 2) {
+                    ptx::umma_commit_pair(&empty[cid % kCommitRing]);
+                  } else {
+                    ptx::umma_commit(&empty[cid % kCommitRing]);
+                  }
+                }
+                ++cid;
+                ea = wrap_inc(ea, R);
+                ++kq;
+                __syncwarp();
+              }
+            }
+          }
         }
         if (lane == 0) {
           for (int j = 0; j <= wide; ++j) {
@@ -1535,7 +1646,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       const bool v8ok = ((reinterpret_cast<uintptr_t>(st.c) | (st.ldc * sizeof(T))) & 31) == 0;
       constexpr int G = C::kEpiGroups;
       if (C::kChunked && !QD &&
-          (bal ? brole != 0 : (t.z >= 2 && t.z <= 4 && !((p.flags >> 29) & 1)))) {
+          (bal ? brole != 0
+               : (!((p.flags >> 29) & 1) &&
+                  (st.red_mma ? (t.z >= 2 && t.tz < t.z - 1) : (t.z >= 2 && t.z <= 4))))) {
         // Split-K slice (the reference's z > 1) of a CTA-pair tile, reduced into the
         // accumulator of the LAST slice to arrive (per tile half = per CTA): each slice
         // takes an arrival index from cnt[half]; the first z - 1 write their fp32 partial
@@ -1579,6 +1692,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         int arrival;
         if (bal) {
           arrival = brole == 1 ? 0 : nparts;
+        } else if (st.red_mma) {
+          // a writer slice (the owner, the last slice, reduces on the tensor cores and
+          // takes the plain epilogue below)
+          arrival = t.tz;
         } else if (t.z > 2) {
           arrival = t.tz == t.z - 1 ? nparts : t.tz;  // static owner: the last slice
         } else {
@@ -1597,11 +1714,20 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
               uint32_t r[16];
               ptx::tmem_ld_32x32b_x16(tcol(x), r);
               ptx::tmem_ld_wait();
-              if (mine_ok) {
+              if (mine_ok && !st.red_mma) {
                 uint4* d = reinterpret_cast<uint4*>(mine + (static_cast<size_t>(x / 16) * 512 + rl_row) * 4);
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                   d[q * 128] = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+              } else if (mine_ok) {
+                // row-major [128 rows][tile columns] fp32: the owner's reduction boxes,
+                // written evict_last so they are still in L2 when the owner streams them
+                float* d = mine + static_cast<size_t>(rl_row) * acc_cols + x;
+                const uint64_t pel = ptx::policy_evict_last();
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  ptx::st_global_v4_hint(d + 4 * q, make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2],
+                                                               r[4 * q + 3]), pel);
               }
             }
             release_slot(j);
@@ -1611,6 +1737,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
           if (threadIdx.x == 128) {
             if (uleader && p.trace != nullptr)  // partial written (extension)
               trace_event(p, ptx::global_timer(), 9, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
+            ptx::fence_proxy_async_global();  // the owner reads the plane with TMA
             ptx::atom_add_release_gpu(rdy, 1);
           }
         } else {
@@ -1703,7 +1830,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
             release_slot(j);
           }
         }
-      } else if (t.z > 1) {
+      } else if (t.z > 1 && !(C::kChunked && !QD && st.red_mma && !bal && t.tz == t.z - 1 &&
+                                !((p.flags >> 29) & 1))) {
+        // (a tensor-core-reduced owner slice — its accumulator already holds every slice —
+        // takes the plain epilogue below)
         // Split-K slice (the reference's z > 1) of a normal tile: publish this CTA's fp32
         // partial rows, count arrivals per (tile, CTA); the last slice to arrive sums all
         // partials, applies the epilogue and stores. Every slice still posts once below

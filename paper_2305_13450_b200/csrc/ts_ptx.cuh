@@ -220,6 +220,11 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 
 // Order this thread's generic-proxy view of global memory before its later async-proxy
 // (TMA) accesses, and vice versa.
+// generic-proxy shared-memory writes -> async proxy (tcgen05.mma / TMA reads of them)
+__device__ __forceinline__ void fence_proxy_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -554,6 +559,41 @@ __device__ __forceinline__ uint64_t smem_desc_k_sw128(uint32_t smem_addr) {
 // Instruction descriptor for kind::f16, fp32 accumulate, both operands K-major.
 //   [4,6) D fmt = 1 (f32), [7,10) A fmt, [10,13) B fmt (0 f16, 1 bf16),
 //   [15] A major = 0, [16] B major = 0, [17,23) N>>3, [24,29) M>>4.
+// Instruction descriptor for kind::tf32 (A, B tf32 = 2, D f32), both K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t m, uint32_t n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
+
+// One 32-deep K block of kind::tf32 MMAs (4 x K = 8, 32 bytes each) accumulating into D:
+// the split-K reduction D += P x I over a 32-column group of a partial plane P.
+template <int CG>
+__device__ __forceinline__ void umma_tf32_kblock(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                                 uint32_t idesc) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "{\n\t.reg .pred t;\n\t"
+        "setp.eq.b32 t, %3, %3;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, t;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %4, %5, %3, t;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %6, %7, %3, t;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %8, %9, %3, t;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "l"(adesc + 2), "l"(bdesc + 2), "l"(adesc + 4),
+        "l"(bdesc + 4), "l"(adesc + 6), "l"(bdesc + 6)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred t;\n\t"
+        "setp.eq.b32 t, %3, %3;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %4, %5, %3, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %6, %7, %3, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %8, %9, %3, t;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "l"(adesc + 2), "l"(bdesc + 2), "l"(adesc + 4),
+        "l"(bdesc + 4), "l"(adesc + 6), "l"(bdesc + 6)
+        : "memory");
+  }
+}
+
 __host__ __device__ constexpr uint32_t idesc_f16(uint32_t m, uint32_t n, uint32_t ab_fmt) {
   return (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }

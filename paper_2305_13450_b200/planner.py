@@ -12,6 +12,7 @@ from (reference gpu.waves at GpuConfig(148)).
 from __future__ import annotations
 
 import itertools
+import statistics
 
 import torch
 
@@ -139,6 +140,27 @@ def candidates(m: int, mode: str, n2: int | None = None, units: int = 74,
     return out
 
 
+# split-K reduction variants (chain flags): the owner slice's tensor-core reduction
+# (D += P x I over TMA-streamed partial planes, bit 27) and every slice publishing a plane
+# for the last arriver to sum (bit 29); neither wins everywhere (profiles/r02x_reduce_ab.txt)
+REDUCE_TC, REDUCE_ALL_PLANES = 1 << 27, 1 << 29
+
+
+def with_reduce_variants(cands):
+    """Each split-K candidate of a CTA-pair 256-wide chain also with the two alternative
+    reduction paths."""
+    out = []
+    for kw in cands:
+        out.append(kw)
+        split = kw.get("prod_splits", 1) > 1 or kw.get("cons_splits", 1) > 1 or \
+            kw.get("cons_tail", (0, 1))[0] > 0
+        if split and kw.get("cta_group") == 2 and kw.get("tile_n") == 256 and \
+                kw.get("cluster_pairs", 1) == 1 and not kw.get("swap_ab"):
+            for fl in (REDUCE_TC, REDUCE_ALL_PLANES):
+                out.append(dict(kw, extra_flags=kw.get("extra_flags", 0) | fl))
+    return out
+
+
 def describe(kw) -> dict:
     co = kw.get("cons_order", RowMajor())
     swap = kw.get("swap_ab", False)
@@ -156,6 +178,9 @@ def describe(kw) -> dict:
         d["consumer_tail"] = list(kw["cons_tail"])  # (tiles, split-K slices) of the last wave
     if kw.get("cluster_pairs", 1) == 2:
         d["cluster_pairs"] = 2  # the 256 x 512 tile on two multicast-sharing CTA pairs
+    fl = kw.get("extra_flags", 0)
+    if fl & (REDUCE_TC | REDUCE_ALL_PLANES):
+        d["reduce"] = "tensor-core" if fl & REDUCE_TC else "all-planes"
     return d
 
 
@@ -171,7 +196,8 @@ def pick_mlp(x, w1, w2, mode="fused", tie=0.015):
     timed = []
     with torch.cuda.device(x.device):
         units, qd_units = chain_units(), chain_units(cluster_pairs=2)
-    for kw in candidates(x.shape[0], mode, n2=w2.shape[0], units=units, qd_units=qd_units):
+    for kw in with_reduce_variants(candidates(x.shape[0], mode, n2=w2.shape[0], units=units,
+                                              qd_units=qd_units)):
         ch = MlpChain(x, w1, w2, **kw)
         us = _time(ch)
         _check_watchdog(ch, kw)
@@ -179,6 +205,22 @@ def pick_mlp(x, w1, w2, mode="fused", tie=0.015):
         timed.append((us, kw))
         if us < best_us:
             best, best_us = kw, us
+    # Candidates within a few percent of each other are separated by box noise (the power
+    # cap moves the SM clock between measurements): re-time the fastest four round-robin,
+    # three rounds of 20 chains, and keep the best median.
+    top = sorted(timed, key=lambda t: t[0])[:4]
+    if len(top) > 1:
+        chains = [(kw, MlpChain(x, w1, w2, **kw)) for _, kw in top]
+        runs = {id(kw): [] for kw, _ in chains}
+        for _ in range(3):
+            for kw, ch in chains:
+                runs[id(kw)].append(_time(ch, iters=20, warm=3))
+        for kw, ch in chains:
+            _check_watchdog(ch, kw)
+        scored = [(statistics.median(runs[id(kw)]), i, kw) for i, (kw, _) in enumerate(chains)]
+        best_us, _, best = min(scored, key=lambda t: (t[0], t[1]))
+        timed = [(statistics.median(runs[id(kw)]) if id(kw) in runs else us, kw)
+                 for us, kw in timed]
     if x.shape[0] >= 512 and best is not None and best.get("prod_splits", 1) > 1:
         lean = [(us, kw) for us, kw in timed
                 if kw.get("prod_splits", 1) == 1 and not kw.get("swap_ab", False)

@@ -131,6 +131,20 @@ def test_gpt3_mlp_fixed_plans(b, kw):
     run_mlp(b, dict(kw, mode="fused"))
 
 
+REDUCE = [(b, kw) for b, kw in FIXED if kw.get("cta_group") == 2 and kw.get("tile_n") == 256
+          and kw.get("cluster_pairs", 1) == 1
+          and (kw.get("prod_splits", 1) > 1 or kw.get("cons_splits", 1) > 1 or "cons_tail" in kw)]
+
+
+@pytest.mark.parametrize("fl", [planner.REDUCE_TC, planner.REDUCE_ALL_PLANES],
+                         ids=["tensor-core", "all-planes"])
+@pytest.mark.parametrize("b,kw", REDUCE, ids=[f"B{b}-{i}" for i, (b, _) in enumerate(REDUCE)])
+def test_gpt3_mlp_reduce_variants(b, kw, fl):
+    """The split-K reduction variants the planner times (tensor-core owner reduction over
+    TMA-streamed planes; every slice publishing a plane) on the benchmarked split plans."""
+    run_mlp(b, dict(kw, mode="fused", extra_flags=fl))
+
+
 @pytest.mark.parametrize("b", [1, 64, 256, 1024, 2048])
 def test_gpt3_mlp_planner_pick(b):
     """Whatever the planner picks on this device (what bench.py runs), fused and stream."""
