@@ -124,6 +124,17 @@ typedef enum {
                               inputs that arrive row by row (MlpChain.run_host); every
                               consumer item is still claimed after the producer items
                               it waits on                                               */
+  TS_FLAG_CONV_HALO = 32,    /* convolution stages with Cin = Cout = 64 (cta_group 1,
+                              tile_n 64): stage each tile's input rows + 3x3 halo ONCE in
+                              shared memory (a 4-D TMA box; zero padding from the
+                              out-of-bounds fill) and address the nine tap-shifted A views
+                              as descriptor offsets of whole 128-B pixel rows, with the
+                              layer's weight taps resident — instead of one im2col box per
+                              tap (9x the input bytes). Tiles are 128 positions of an image
+                              in a width-padded order (row stride W + 2; two junk columns
+                              per row, not stored) or, for wide images, 128 positions of one
+                              row; the stage grid is N x tiles-per-image. Every conv stage of
+                              the chain must qualify                                         */
   TS_FLAG_BALANCED = 16      /* fused CTA-pair 256-wide GeMM chains: static stream-K
                               schedule. Each stage's flattened (tile in claim order,
                               K-block) space is cut into one equal range per work unit

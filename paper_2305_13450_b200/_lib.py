@@ -26,6 +26,7 @@ TS_MODE_STREAM, TS_MODE_FUSED, TS_MODE_CORESIDENT = range(3)
 TS_STAGE_GEMM, TS_STAGE_ATTN_DOT, TS_STAGE_CONV2D, TS_STAGE_ALLREDUCE = range(4)
 TS_FLAG_KEEP_SEMS, TS_FLAG_NO_REORDER, TS_FLAG_NO_WATCHDOG, TS_FLAG_ROW_INTERLEAVE = 1, 2, 4, 8
 TS_FLAG_BALANCED = 16
+TS_FLAG_CONV_HALO = 32
 
 TS_MAX_STAGES = 4
 TS_MAX_DEPS = 4

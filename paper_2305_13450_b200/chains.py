@@ -204,14 +204,17 @@ class ConvChain:
                  cta_group: int = 1, keep_sems: bool = False, num_ctas: int = 0,
                  extra_flags: int = 0, prod_order: TileOrder = RowMajor(),
                  cons_order: TileOrder = RowMajor(), act: str = "relu", prod_splits: int = 1,
-                 cons_splits: int = 1):
+                 cons_splits: int = 1, halo: bool = False):
+        """``halo=True`` (64-channel layers, tile_n=64, cta_group=1): each tile's input
+        rows + halo are staged once and the nine taps read shifted views of them
+        (TS_FLAG_CONV_HALO)."""
         from .policies import Conv2DTileSync
         n, h, w, _ = x.shape
         self.x, self.w1, self.w2 = x, w1, w2
         self.h = torch.empty(n, h, w, w1.shape[0], dtype=x.dtype, device=x.device)
         self.y = torch.empty(n, h, w, w2.shape[0], dtype=x.dtype, device=x.device)
         self.cs = CuSync(tile_n=tile_n, mode=mode, keep_sems=keep_sems, num_ctas=num_ctas,
-                         cta_group=cta_group, extra_flags=extra_flags)
+                         cta_group=cta_group, extra_flags=extra_flags, conv_halo=halo)
         self.prod = self.cs.stage_conv(x, w1, self.h, epilogue=act, order=prod_order, id="conv1",
                                        splits=prod_splits)
         self.cons = self.cs.stage_conv(self.h, w2, self.y, order=cons_order, id="conv2",

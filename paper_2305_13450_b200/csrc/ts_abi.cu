@@ -151,6 +151,38 @@ int make_tmap_ws(CUtensorMap* m, const float* ptr, long long rows, int cols) {
   return TS_OK;
 }
 
+// Halo-staged convolution window: NHWC input as a 4-D (C, W, H, N) tensor, box (64
+// channels, bw pixels, bh rows, 1 image), 128-B swizzle (one pixel = one 128-B row); boxes
+// start at column -1 / row -1, the out-of-bounds fill supplies the zero padding.
+int make_tmap_window(CUtensorMap* m, const void* ptr, int n, int h, int w, int ldc_px, int dtype,
+                     int bw, int bh) {
+  const TmapKey key{ptr, {3, n, h, w, static_cast<long long>(ldc_px) * 4 + dtype,
+                          (static_cast<long long>(bw) << 16) | bh}};
+  if (const CUtensorMap* hit = g_tmaps.find(key)) {
+    *m = *hit;
+    return TS_OK;
+  }
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(TS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  cuuint64_t dims[4] = {64, static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
+                        static_cast<cuuint64_t>(n)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(ldc_px) * 2,
+                           static_cast<cuuint64_t>(ldc_px) * 2 * w,
+                           static_cast<cuuint64_t>(ldc_px) * 2 * w * h};
+  cuuint32_t box[4] = {64, static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, dtype == TS_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   4, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TS_ERR_CUDA, "cuTensorMapEncodeTiled (conv window) failed (%d) n=%d h=%d w=%d", (int)r,
+                n, h, w);
+  g_tmaps.put(key, *m);
+  return TS_OK;
+}
+
 using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                     const cuuint64_t*, const cuuint64_t*, const int*,
                                     const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
@@ -330,6 +362,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
   p->ctl = d->scratch;
   p->coresident = 0;
   p->balanced = (d->flags & TS_FLAG_BALANCED) ? 1 : 0;
+  p->claim_batch = (d->flags & TS_FLAG_CONV_HALO) ? 2 : 1;
   p->trace = static_cast<ts_trace_rec*>(d->trace);
   p->trace_cap = d->trace ? d->trace_cap : 0;
   const int dtype = d->stages[0].dtype;
@@ -502,10 +535,44 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
       sp.conv_cin = st.k / 9;
       sp.conv_subs = 1;  // K channel tile = 64 unless a producer's column tile sets it
       sp.halo = (st.conv_w + 1 + tile_m - 1) / tile_m;
-      if (sp.halo > 2)
+      if (d->flags & TS_FLAG_CONV_HALO) {
+        // halo-staged tiles (see StageParams::hmode): Cin = Cout = 64 on single-CTA 64-wide
+        // tiles; rows mode while the window (rows the 128 positions span + 2 halo rows) fits
+        // 56 KB, else one 128-position segment of a row per tile
+        if (cg != 1 || bn != 64 || swap || st.k != 9 * 64 || st.n != 64 || splits != 1 ||
+            st.conv_w + 2 > 256 || st.tile_n != 0)
+          return fail(TS_ERR_CONFIG, "stage %d: halo-staged convolution needs Cin = Cout = 64, "
+                      "cta_group 1, tile_n 64, no split-K, width <= 254", s);
+        const int srow = st.conv_w + 2;
+        if (srow <= 128) {
+          // rows mode: a tile = the whole width-padded rows that fit 128 positions
+          sp.hmode = 1;
+          sp.hs = srow;
+          sp.hrpt = 128 / srow < st.conv_h ? 128 / srow : st.conv_h;
+          sp.hrows = sp.hrpt + 2;
+          sp.htpi = (st.conv_h + sp.hrpt - 1) / sp.hrpt;
+          sp.htpr = 0;
+        } else {
+          sp.hmode = 2;
+          sp.hs = 130;
+          sp.hrows = 3;
+          sp.hrpt = 1;
+          sp.htpr = (st.conv_w + 127) / 128;
+          sp.htpi = st.conv_h * sp.htpr;
+        }
+        sp.hbytes = sp.hrows * sp.hs * 128;
+        sp.hwin = (sp.hbytes + 1023) / 1024 * 1024;
+        sp.hnb = (196608 - 9 * 8192) / sp.hwin;  // the BN = 64 kernel's operand ring
+        if (sp.hnb > 4) sp.hnb = 4;
+        if (sp.hnb < 2)
+          return fail(TS_ERR_CONFIG, "stage %d: conv window of %d bytes too large", s, sp.hbytes);
+        sp.halo = 0;  // the window waits cover the halo rows
+      } else if (sp.halo > 2) {
         return fail(TS_ERR_CONFIG, "stage %d: image width %d needs a 3x3 halo of %d row tiles "
                     "(at most 2; use larger tiles)", s, st.conv_w, sp.halo);
+      }
     }
+    if (sp.hmode) sp.grid_x = st.conv_n * sp.htpi;  // per-image re-tiling (halo conv)
     sp.splits = splits;
     sp.ws = st.workspace;
     sp.cnt = st.counters;
@@ -550,6 +617,11 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     if (with_tmaps) {
       // activations: box rows = 128 per CTA (normal) or tile_n (swapped);
       // weights: box rows = tile_n / cta_group (normal) or 128 (swapped)
+      if (sp.hmode) {
+        int rr = make_tmap_window(&sp.tmap_win, st.a, st.conv_n, st.conv_h, st.conv_w, st.lda,
+                                  st.dtype, sp.hs, sp.hrows);
+        if (rr) return rr;
+      }
       int r = conv ? make_tmap_im2col(&sp.tmap_a, st.a, st.conv_n, st.conv_h, st.conv_w, st.k / 9,
                                       st.lda, st.dtype, 128)
                    : make_tmap(&sp.tmap_a, st.a, st.m, st.k, st.lda, st.dtype, swap ? bn : 128);

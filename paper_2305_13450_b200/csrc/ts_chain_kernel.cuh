@@ -115,6 +115,17 @@ struct StageParams {
   // last-wave balancing: the last tail_tiles tiles (claim order) run as tail_splits
   // split-K slices each; items = tiles - tail_tiles + tail_tiles * tail_splits
   int tail_tiles, tail_splits;
+  // halo-staged convolution (TS_FLAG_CONV_HALO; Cin = Cout = 64, one CTA per 128-row
+  // tile): the tile's input rows + 3x3 halo are loaded ONCE per tile into shared memory
+  // (4-D TMA box, zero padding by out-of-bounds fill) and the nine tap-shifted A views are
+  // UMMA descriptors offset by whole 128-B pixel rows; the layer's 9 weight taps stay
+  // resident. hmode 1: a tile = 128 consecutive positions of one image in padded order
+  // (row stride hs = W + 2, two junk columns per row); 2: a tile = 128 positions of one row
+  // (hs = 130). 0: the im2col-per-tap path.
+  int hmode, hs, htpi, htpr, hrows, hbytes;
+  int hrpt;      // rows mode: image rows per tile (a tile = hrpt x hs positions)
+  int hnb, hwin;  // window buffers in flight and their stride (bytes, 1024-aligned)
+  CUtensorMap tmap_win;  // (C, W, H, N) box (64, hs, hrows, 1), 128-B swizzle
 };
 
 struct DepParams {
@@ -140,6 +151,7 @@ struct ChainParams {
   int* ctl;
   int coresident;
   int balanced;   // TS_FLAG_BALANCED: static stream-K assignment (0 = dynamic claims)
+  int claim_batch;  // items per claim (halo-conv kernels: short tiles, one atomic per 2-4)
   ts_trace_rec* trace;
   int trace_cap;
   int flags;
@@ -208,7 +220,13 @@ struct Cfg {
   static constexpr int kIdentOff = kStageOff + (kEpiThreads / 32) * TS_STAGE_WARP_BYTES;
   static constexpr int kBarOffset = kChunked ? kIdentOff + 4096 : kStages * kStageBytes;
   // K-block full, commit-group empty; tmem full/empty x2; tile ring full/empty; peer_done
-  static constexpr int kNumBars = kFullRing + kCommitRing + 4 + 2 * kTileRing + kPeerRing + 2;
+  // halo conv (hmode != 0, CG = 1, BN = 64): 9 weight taps (72 KB) then 2-4 window
+  // buffers (StageParams::hnb x hwin bytes) in the (unused) operand ring
+  static constexpr int kHaloRegion = kStages * kStageBytes;
+  static constexpr bool kHaloOk = !kChunked && CG == 1 && !SW && BN == 64 &&
+                                  9 * 8192 + 2 * 50176 <= kHaloRegion;
+  static constexpr int kNumBars =
+      kFullRing + kCommitRing + 4 + 2 * kTileRing + kPeerRing + 2 + 9;
   // + tile ring ids, TMEM slot, flags and the last-arriver dot list (64 ints), ring-entry
   // owners (commit group that last read each entry)
   static constexpr int kSmemBytes =
@@ -651,6 +669,45 @@ __device__ __forceinline__ void allreduce_rows(const ChainParams& p, const Stage
 // next (a 256 x 512 tile on one pair fills all of TMEM). Ring entries are freed by both
 // pairs' MMA commits (empty barriers count 2); the cluster leader claims items, hands the
 // id to the other three CTAs and posts once all four have stored.
+// Halo-staged convolution geometry (StageParams::hmode). For tile tx: image n, first
+// image row h0, first padded column w0 and the A base pixel inside the window buffer
+// (the window starts at padded column 0 / w0 - 1 of image row h0 - 1).
+struct HaloTile {
+  int n, h0, w0, base;
+};
+
+__device__ __forceinline__ HaloTile halo_tile(const StageParams& st, int tx) {
+  HaloTile h;
+  h.n = tx / st.htpi;
+  const int lt = tx - h.n * st.htpi;
+  if (st.hmode == 1) {
+    h.h0 = lt * st.hrpt;
+    h.w0 = 0;
+    h.base = 0;
+  } else {
+    h.h0 = lt / st.htpr;
+    h.w0 = (lt - h.h0 * st.htpr) * 128;
+    h.base = 0;
+  }
+  return h;
+}
+
+// Output pixel of accumulator row m of halo tile `ht` (or -1: a junk position of the
+// padded order / past the image edge).
+__device__ __forceinline__ int halo_pixel(const StageParams& st, const HaloTile& ht, int m) {
+  int h, w;
+  if (st.hmode == 1) {
+    if (m >= st.hrpt * st.hs) return -1;  // rows of the tile: hrpt x hs positions
+    h = ht.h0 + m / st.hs;
+    w = m % st.hs;
+  } else {
+    h = ht.h0;
+    w = ht.w0 + m;
+  }
+  if (h >= st.conv_h || w >= st.conv_w) return -1;
+  return (ht.n * st.conv_h + h) * st.conv_w + w;
+}
+
 // Split-K owner, producer side: wait until the other slices' fp32 partial planes of this
 // CTA's rows are written, then stream them in as 32-column x 128-row boxes (the A operand
 // of the tensor-core reduction D += P x I), one ring chunk and one commit group per box.
@@ -722,7 +779,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
   uint64_t* peer_done = ti_empty + kTileRing;
   uint64_t* dot_msg = peer_done + kPeerRing;  // peer CTA: leader's list of released dot tiles
   uint64_t* dot_done = dot_msg + 1;           // leader: peer finished its half of them
-  int* ti_item = reinterpret_cast<int*>(dot_done + 1);
+  // halo conv: weights landed, window landed [2], window consumed by the MMAs [2]
+  uint64_t* hw_full = dot_done + 1;
+  uint64_t* win_full = hw_full + 1;    // [4]
+  uint64_t* win_empty = win_full + 4;  // [4]
+  int* ti_item = reinterpret_cast<int*>(win_empty + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ti_item + kTileRing);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   int* split_flag = last_flag + 1;
@@ -757,6 +818,11 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       ptx::mbar_init(&peer_done[i], NP * CG > 1 ? NP * CG - 1 : 1);  // the other CTAs' stores
     ptx::mbar_init(dot_msg, 1);
     ptx::mbar_init(dot_done, 1);
+    ptx::mbar_init(hw_full, 1);
+    for (int i = 0; i < 4; ++i) {
+      ptx::mbar_init(&win_full[i], 1);
+      ptx::mbar_init(&win_empty[i], 1);
+    }
     for (int i = 0; i < kTileRing; ++i) {
       ptx::mbar_init(&ti_full[i], 1);
       // every pair's MMA warp + every epilogue warp of the cluster + the other CTAs'
@@ -860,6 +926,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         }
         owner[e] = static_cast<int>(cid);
       };
+      int hi = 0, pw_stage = -1;  // halo conv: windows issued, stage of the resident weights
+      int cb_next = 0, cb_left = 0;  // claim batching (halo-conv kernels)
       // balanced schedule state (shared memory: the scheduler lane's registers are the
       // kernel's tightest): stage, next and end position in the stage's flattened space
       if (bal) {
@@ -902,6 +970,17 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
             bst[0] = bs;
             bst[1] = bpos;
             bst[2] = bend;
+          } else if (C::kHaloOk && p.claim_batch > 1) {
+            // short halo-conv tiles: one claim RMW (a loaded L2 round trip in the
+            // scheduler lane) per claim_batch consecutive items
+            if (cb_left == 0) {
+              cb_next = p.item_lo + atomicAdd(&p.ctl[0], p.claim_batch);
+              cb_left = p.claim_batch;
+            }
+            g = cb_next < p.item_hi ? cb_next : -1;
+            ++cb_next;
+            --cb_left;
+            if (g < 0) cb_left = 0;
           } else {
             g = p.item_lo + atomicAdd(&p.ctl[0], 1);
             if (g >= p.item_hi) g = -1;
@@ -930,6 +1009,62 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
           trace_event(p, ptx::global_timer(), 0, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
         if (st.kind == kStageDot || st.kind == kStageAllReduce)
           continue;  // pointwise stages: the epilogue warps run them
+        if constexpr (C::kHaloOk) {
+          if (st.hmode) {
+            // (1) the stage's nine weight taps, resident for all its tiles: reload once the
+            // MMAs of every earlier window (the old weights' readers) have completed
+            if (t.s != pw_stage) {
+              for (int j = hi - st.hnb; j < hi; ++j)
+                if (j >= 0) ptx::mbar_wait(&win_empty[j % st.hnb], (j / st.hnb) & 1);
+              ptx::mbar_arrive_expect_tx(hw_full, 9 * 8192);
+              for (int tap = 0; tap < 9; ++tap)
+                ptx::tma_load_2d(smem + tap * 8192, &st.tmap_b, hw_full, tap * kBK, t.ty * 64,
+                                 ptx::policy_evict_last());
+              pw_stage = t.s;
+            }
+            const HaloTile ht = halo_tile(st, t.tx);
+            // (2) stage.wait(): the producer tiles whose rows the window covers (the
+            // reference's Conv2DTileSync wait of k-step 0 is tile tx itself; the 3x3 halo
+            // rows ride along untraced)
+            const int d = st.in_dep;
+            if (d >= 0 && !((p.flags >> 12) & 1)) {
+              const DepParams& dp = p.dep[d];
+              if (uleader)
+                trace_event(p, ptx::global_timer(), 1, t.s, t.tb, 0, d, t.tx, dp.pgz, t.tx, t.ty, t.tz);
+              const int base_t = ht.n * st.htpi;
+              auto wait_tile = [&](int u) {
+                if (!((done_mask >> d) & 1) &&
+                    sem_wait_dep(p, d, dp.sem + u, dp.pgz, nullptr, 0, nullptr, 0, nullptr, 0,
+                                 nullptr, 0))
+                  done_mask |= 1u << d;
+              };
+              const int hlo = ht.h0 > 0 ? ht.h0 - 1 : 0;
+              if (st.hmode == 1) {
+                const int hhi0 = ht.h0 + st.hrpt;  // last input row the window reads
+                const int hhi = hhi0 < st.conv_h - 1 ? hhi0 : st.conv_h - 1;
+                for (int u = hlo / st.hrpt; u <= hhi / st.hrpt; ++u) wait_tile(base_t + u);
+              } else {
+                const int hhi = ht.h0 + 1 < st.conv_h - 1 ? ht.h0 + 1 : st.conv_h - 1;
+                const int s0 = ht.w0 > 0 ? (ht.w0 - 1) / 128 : 0;
+                const int s1 = (ht.w0 + 128 < st.conv_w - 1 ? ht.w0 + 128 : st.conv_w - 1) / 128;
+                for (int hh = hlo; hh <= hhi; ++hh)
+                  for (int sg = s0; sg <= s1; ++sg) wait_tile(base_t + hh * st.htpr + sg);
+              }
+              if (uleader)
+                trace_event(p, ptx::global_timer(), 2, t.s, t.tb, 0, d, t.tx, dp.pgz, t.tx, t.ty, t.tz);
+              ptx::fence_proxy_async_global();
+            }
+            // (3) the window: input rows h0 - 1 .. h0 + hrows - 2 (+ halo columns), once
+            const int b = hi % st.hnb;
+            if (hi >= st.hnb) ptx::mbar_wait(&win_empty[b], ((hi / st.hnb) & 1) ^ 1);
+            ptx::mbar_arrive_expect_tx(&win_full[b], st.hbytes);
+            ptx::tma_load_4d(smem + 9 * 8192 + b * st.hwin, &st.tmap_win, &win_full[b], 0,
+                             st.hmode == 1 ? -1 : ht.w0 - 1, ht.h0 - 1, ht.n,
+                             ptx::policy_evict_normal());
+            ++hi;
+            continue;
+          }
+        }
         // activation (dependent) and weight (independent) tile rows of this CTA
         const int act_row = SW ? t.tx * BN : t.tx * C::kTileM + static_cast<int>(rank) * 128;
         // a double-width tile's second B box (output columns [BN, 2 BN) of the pair
@@ -1210,6 +1345,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       uint32_t cid = 0;   // commit group
       const int group = commit_group(p.flags);
       uint32_t u = 0;  // TMEM accumulator-slot uses (a double-width tile takes two)
+      int hm = 0, mw_stage = -1, mw_count = 0;  // halo conv: windows, resident-weight loads
 #pragma unroll 1
       for (int it = 0;; ++it) {
         int kbr;
@@ -1218,8 +1354,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         const StageParams& sp = p.st[stage_of(p, g)];
         if (sp.kind == kStageDot || sp.kind == kStageAllReduce)
           continue;  // no MMA, no accumulator buffer
-        const int kblocks = bal ? (kbr & 0xffff) - (kbr >> 16)
-                                : sp.k_blocks / item_slices(sp, g - sp.item_begin);
+        const int kblocks = (C::kHaloOk && sp.hmode) ? 0
+                            : bal ? (kbr & 0xffff) - (kbr >> 16)
+                                  : sp.k_blocks / item_slices(sp, g - sp.item_begin);
         const int wide = (C::kChunked && !QD) ? sp.wide : 0;
         // instruction descriptor: N = the stage's columns per MMA (chunked stages)
         const uint32_t idesc = C::kChunked ? ptx::idesc_f16(128 * CG, sp.half_n, AbFormat<T>::value)
@@ -1233,6 +1370,43 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         const bool tr = p.trace != nullptr;
         const bool no_mma = (p.flags >> 13) & 1;  // diagnostic only: skip the MMAs
         uint64_t starve_ns = 0;  // time this tile's MMAs waited for operand stages
+        if constexpr (C::kHaloOk) {
+          if (sp.hmode) {
+            // halo conv tile: nine taps x four K = 16 MMAs over one staged window; tap
+            // (r, s)'s A is the window shifted by r window rows + s pixels (whole 128-B
+            // rows: the 128-B swizzle is address based, so any row offset is a valid
+            // K-major descriptor start), B the resident tap weights
+            const int stg_i = stage_of(p, g);
+            if (stg_i != mw_stage) {
+              ptx::mbar_wait(hw_full, mw_count & 1);
+              ++mw_count;
+              mw_stage = stg_i;
+            }
+            const int b = hm % sp.hnb;
+            ptx::mbar_wait(&win_full[b], (hm / sp.hnb) & 1);
+            ptx::tc_fence_after();
+            if (lane == 0) {
+              const HaloTile ht = halo_tile(sp, decode(p, g).tx);
+              if (tr) {
+                const Tile t5 = decode(p, g);
+                trace_event(p, ptx::global_timer(), 5, t5.s, t5.tb, -1, -1, -1, -1, t5.tx, t5.ty);
+              }
+              const uint32_t wb = ptx::smem_u32(smem + 9 * 8192 + b * sp.hwin);
+#pragma unroll 1
+              for (int tap = 0; tap < 9; ++tap) {
+                const int r = tap / 3, s = tap - 3 * (tap / 3);
+                const uint64_t ad = ptx::smem_desc_k_sw128(wb + (ht.base + r * sp.hs + s) * 128);
+                const uint64_t bdd = ptx::smem_desc_k_sw128(ptx::smem_u32(smem + tap * 8192));
+                // (one accumulator: a second one for alternating taps measured no faster and
+                // doubles the epilogue's TMEM reads, the other pacing resource)
+                if (!no_mma) ptx::umma_f16_kblock<CG>(d_tmem, ad, bdd, kIdesc, tap != 0);
+              }
+              ptx::umma_commit(&win_empty[b]);
+            }
+            ++hm;
+            __syncwarp();
+          }
+        }
 #pragma unroll 1
         for (int kb = 0, gi = 0; kb < kblocks; ++kb) {
           uint64_t* fb = &full[kq % kFullRing];
@@ -1272,7 +1446,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
               const uint32_t a_addr = ptx::smem_u32(sA + rs * C::kABytes);
               const uint32_t b_addr = ptx::smem_u32(sB + rs * C::kBBytes);
               if (no_mma) {
-              } else if constexpr (C::kAcc > 1) {
+              } else if constexpr (SW && C::kAcc > 1) {
                 // rotate independent accumulators (sub-step `step` -> step % kAcc), the
                 // K-block's four MMAs in one issue sequence
                 const int step = kb * (kBK / 16);
@@ -1637,8 +1811,16 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         }
       } else {
       const int row = t.tx * C::kTileM + static_cast<int>(rank) * 128 + ew * 32 + lane;
-      const bool row_ok = row < st.m;
+      bool row_ok = row < st.m;
       T* crow = reinterpret_cast<T*>(st.c) + static_cast<size_t>(row) * st.ldc;
+      if constexpr (C::kHaloOk) {
+        if (st.hmode) {
+          // halo conv: accumulator row -> output pixel (junk positions are not stored)
+          const int px = halo_pixel(st, halo_tile(st, t.tx), ew * 32 + lane);
+          row_ok = px >= 0;
+          crow = reinterpret_cast<T*>(st.c) + static_cast<size_t>(px < 0 ? 0 : px) * st.ldc;
+        }
+      }
       const int acc_cols = hn << wide;  // accumulator columns of this tile (this pair's)
       // first output column of this pair's accumulator (QD: the pair's half of the unit)
       const int col0 = QD ? (2 * t.ty + static_cast<int>(pair)) * acc_cols : t.ty * acc_cols;
@@ -2075,9 +2257,15 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
               // an all-reduce consumer reads this semaphore (and the tile) from peer GPUs
               const bool sys = p.st[dp.consumer].kind == kStageAllReduce;
               if (sys) __threadfence_system();
-              const int old = sys ? ptx::atom_add_release_sys(dp.sem + idx, 1)
-                                  : ptx::atom_add_release_gpu(dp.sem + idx, 1);
-              ptx::atom_add_release_gpu(p.scratch + kDoneBase + d, 1);
+              int old = 0;
+              if (sys) {
+                old = ptx::atom_add_release_sys(dp.sem + idx, 1);
+              } else if (p.trace != nullptr || d == st.dot_dep) {
+                old = ptx::atom_add_release_gpu(dp.sem + idx, 1);  // the value is used below
+              } else {
+                ptx::red_add_release_gpu(dp.sem + idx, 1);
+              }
+              ptx::red_add_release_gpu(p.scratch + kDoneBase + d, 1);
               trace_event(p, tnow, 3, t.s, t.tb, -1, d, idx, old + 1, t.tx, t.ty, t.tz);
               if (d == st.dot_dep) {
                 // Which dot tiles of this row did this post complete? (the wait of tile

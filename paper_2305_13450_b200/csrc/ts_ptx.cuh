@@ -178,6 +178,18 @@ __device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap
 // 4-D im2col load (NHWC): `pixelsPerColumn` consecutive pixels of the map's bounding box
 // from (w, h, n), channels [c, c + channelsPerPixel), each pixel shifted by the filter
 // tap offsets (ow, oh); out-of-image pixels read as zero.
+// 4-D tiled box (halo-staged convolution windows: (C, W, H, N), negative / past-the-edge
+// coordinates zero-filled).
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c,
+                                            int w, int h, int n, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
+      "l"(cache_hint)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_im2col(void* dst, const CUtensorMap* m, uint64_t* bar,
                                                 int c, int w, int h, int n, uint16_t ow,
                                                 uint16_t oh, uint64_t cache_hint) {
@@ -245,6 +257,12 @@ __device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
 
 __device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// Release reduction without a returned value (fire and forget: no round trip on the
+// posting thread's critical path).
+__device__ __forceinline__ void red_add_release_gpu(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ int atom_add_release_gpu(int* p, int v) {

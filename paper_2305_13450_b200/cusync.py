@@ -106,7 +106,11 @@ class CuStage:
     @property
     def grid(self) -> Dim3:
         """Tile grid as the reference's Stage.grid sees it: (activation-row tiles,
-        output-column tiles, split-K slices)."""
+        output-column tiles, split-K slices). A halo-staged convolution tiles each image's
+        positions separately (``halo_tiles_per_image``)."""
+        if self.kind == "conv" and self.cs.conv_halo:
+            n, h, w = self.conv
+            return Dim3(n * halo_tiles_per_image(h, w), max(1, self.n // self.width), self.splits)
         return Dim3(-(-self.m // self.cs.tile_m), max(1, self.n // self.width), self.splits)
 
     def flops(self) -> int:
@@ -118,6 +122,17 @@ class CuStage:
         "on")."""
         self.cs.wait_kernel = "on"
         return self
+
+
+def halo_tiles_per_image(h: int, w: int) -> int:
+    """Tiles of one H x W image under TS_FLAG_CONV_HALO (ts_abi.cu build_params): the whole
+    width-padded rows (row stride W + 2) that fit 128 positions while W + 2 <= 128, else
+    128-position segments of each row."""
+    srow = w + 2
+    if srow <= 128:
+        rpt = min(128 // srow, h)
+        return -(-h // rpt)
+    return h * -(-w // 128)
 
 
 @dataclass
@@ -158,6 +173,9 @@ class CuSync:
     # static stream-K schedule (TS_FLAG_BALANCED): every CTA pair runs an equal K-block
     # range of each GeMM stage, tiles split across pairs are reduced by their head segment
     balanced: bool = False
+    # halo-staged convolution stages (TS_FLAG_CONV_HALO: Cin = Cout = 64, cta_group 1,
+    # tile_n 64): each tile's input rows + halo loaded once, tap views by descriptor offset
+    conv_halo: bool = False
     device: torch.device | None = None
     stages: list[CuStage] = field(default_factory=list)
     deps: list[CuDep] = field(default_factory=list)
@@ -474,6 +492,8 @@ class CuSync:
         if self.balanced:
             d.flags |= _lib.TS_FLAG_BALANCED
             self._balanced_buffers(d)
+        if self.conv_halo:
+            d.flags |= _lib.TS_FLAG_CONV_HALO
         if self._scratch is None:
             self._scratch = torch.zeros(_lib.TS_SCRATCH_INTS, dtype=torch.int32,
                                         device=self.device)

@@ -322,6 +322,11 @@ def conv_candidates(c: int, mode: str, m: int = 1 << 30):
             if z > 1 and (tiles * z > 2 * 148 or (9 * c // 64) % z):
                 continue
             out.append(dict(mode=mode, tile_n=tn, cta_group=cg, prod_splits=z, cons_splits=z))
+    if c == 64:
+        # 64-channel layers: each tile's input rows + halo staged once, taps as shifted views
+        # (TS_FLAG_CONV_HALO; 1.8-1.9x the im2col-per-tap tiles at B >= 32, r02y)
+        out.append(dict(mode=mode, tile_n=64, cta_group=1, prod_splits=1, cons_splits=1,
+                        halo=True))
     return out
 
 

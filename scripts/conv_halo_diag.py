@@ -1,0 +1,17 @@
+"""Halo conv pipeline diagnostics: timing with diagnostic flags (bit 13: no MMAs, bit 12:
+no semaphore waits) to see which role paces a tile."""
+import sys
+import torch
+sys.path.insert(0, ".")
+import paper_2305_13450_b200 as ts
+from paper_2305_13450_b200 import planner
+hw, c = 56, 64
+torch.manual_seed(0)
+w1 = (torch.randn(c, 3, 3, c, device="cuda") / (9 * c) ** 0.5).half()
+w2 = (torch.randn(c, 3, 3, c, device="cuda") / (9 * c) ** 0.5).half()
+for b in (128, 256):
+    x = torch.randn(b, hw, hw, c, device="cuda").half()
+    for name, fl, mode in (("fused", 0, "fused"), ("stream", 0, "stream"), ("stream no-mma", 1 << 13, "stream"),
+                           ("fused no-wait", 1 << 12, "fused")):
+        ch = ts.ConvChain(x, w1, w2, tile_n=64, cta_group=1, mode=mode, halo=True, extra_flags=fl)
+        print(f"B={b} {name}: {planner._time(ch, iters=20):.1f} us", flush=True)

@@ -129,6 +129,9 @@ def main() -> None:
         for kw in planner.conv_candidates(c, "fused", b * hw * hw):
             tm = 128 * kw["cta_group"]
             gx = -(-(b * hw * hw) // tm)
+            if kw.get("halo"):  # halo-staged tiles: per-image re-tiling
+                from paper_2305_13450_b200.cusync import halo_tiles_per_image
+                gx = b * halo_tiles_per_image(hw, hw)
             z = kw["prod_splits"]
             g = (gx, c // kw["tile_n"], z)
             add(f"{net}_conv_{hw}x{c}_b{b}", [("conv1", g, 9 * c // kw["tile_n"], rm),
