@@ -82,7 +82,11 @@ def candidates(m: int, mode: str, n2: int | None = None, units: int = 74,
                                 prod_splits=z1, cons_splits=z2))
     for cg, tn in ((2, 256), (1, 256), (2, 128), (1, 128)):
         gx = -(-m // (128 * cg))
-        orders = [RowMajor()] + ([BandedColumnMajor(min(gx, 4))] if gx > 1 else [])
+        # consumer orders: RowMajor, and bands of 2 / 3 / 4 row tiles (a band shares each
+        # weight column block in L2; a narrower band puts the last producer row's tiles
+        # later in the claim order, where they wait less)
+        orders = [RowMajor()] + [BandedColumnMajor(b) for b in sorted({2, 3, min(gx, 4)})
+                                 if 1 < b <= gx]
         # per-stage widths: CTA-pair 256-wide chains may give either stage double-width
         # (256 x 512) tiles — fewer operand bytes per MAC, coarser wave quantization
         # (256 x 384 = two N = 192 MMAs: B=1024's GeMM1 as 64 tiles keeps 64 of 74 pairs
