@@ -125,7 +125,8 @@ class SwigluChain:
                  policy: SyncPolicy = RowSync(), mode: str = "fused", tile_n: int = 256,
                  reorder: bool = True, keep_sems: bool = False, num_ctas: int = 0,
                  cta_group: int = 2, prod_tile_n: int = 0, cons_tile_n: int = 0,
-                 cluster_pairs: int = 1):
+                 cluster_pairs: int = 1, prod_splits: int = 1, cons_splits: int = 1,
+                 extra_flags: int = 0):
         """``prod_tile_n`` = 512 packs gate/up per 512-row block
         (``interleave_gate_up(wg, wu, 512)``); with ``cluster_pairs=2`` each pair holds
         256 accumulator columns, so gate/up are packed per 256 rows
@@ -135,10 +136,13 @@ class SwigluChain:
         self.h = torch.empty(m, f, dtype=x.dtype, device=x.device)
         self.y = torch.empty(m, w_down.shape[0], dtype=x.dtype, device=x.device)
         self.cs = CuSync(tile_n=tile_n, mode=mode, reorder=reorder, keep_sems=keep_sems,
-                         num_ctas=num_ctas, cta_group=cta_group, cluster_pairs=cluster_pairs)
+                         num_ctas=num_ctas, cta_group=cta_group, cluster_pairs=cluster_pairs,
+                         extra_flags=extra_flags)
+        # (split-K under SwiGLU: the tensor-core reduction, extra_flags |= 1 << 27)
         self.prod = self.cs.stage(x, w_gate_up, self.h, epilogue="swiglu", id="gate_up",
-                                  tile_n=prod_tile_n)
-        self.cons = self.cs.stage(self.h, w_down, self.y, id="down", tile_n=cons_tile_n)
+                                  tile_n=prod_tile_n, splits=prod_splits)
+        self.cons = self.cs.stage(self.h, w_down, self.y, id="down", tile_n=cons_tile_n,
+                                  splits=cons_splits)
         self.dep = self.cs.dependency(policy, self.prod, self.cons, operand="a")
 
     def __call__(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:

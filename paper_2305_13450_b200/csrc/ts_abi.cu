@@ -506,8 +506,13 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
     if (st.k % (ts::kBK * splits) != 0)
       return fail(TS_ERR_CONFIG, "stage %d: k=%d is not a multiple of %d x %d split(s)", s, st.k,
                   ts::kBK, splits);
-    if (splits > 1 && !swap && st.epilogue == TS_EPI_SWIGLU)
-      return fail(TS_ERR_CONFIG, "stage %d: split-K has no SwiGLU epilogue", s);
+    // SwiGLU needs gate and up summed before SiLU(g) * u: only the tensor-core reduction
+    // (flag bit 27: the owner slice's accumulator holds the full sum before its plain
+    // epilogue) supports split-K under it
+    if (splits > 1 && !swap && st.epilogue == TS_EPI_SWIGLU &&
+        !(((d->flags >> 27) & 1) && cg == 2 && bn == 256 && np == 1))
+      return fail(TS_ERR_CONFIG, "stage %d: split-K under the SwiGLU epilogue needs the "
+                  "tensor-core reduction (flag bit 27, cta_group 2, tile_n 256)", s);
     if (splits > 1 && (st.workspace == nullptr || st.counters == nullptr))
       return fail(TS_ERR_VALUE, "stage %d: split-K needs a workspace and counters", s);
     const int n_out = st.epilogue == TS_EPI_SWIGLU ? st.n / 2 : st.n;

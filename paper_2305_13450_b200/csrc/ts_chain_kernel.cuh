@@ -2219,8 +2219,13 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
 #pragma unroll 1
           for (int x = lo; x < hi; x += 16) {
             uint32_t ra[16];
-            ptx::tmem_ld_32x32b_x16(tcol(x), ra);
-            ptx::tmem_ld_wait();
+            if ((p.flags >> 24) & 1) {  // diagnostic only (bit 24): no TMEM reads
+#pragma unroll
+              for (int q = 0; q < 16; ++q) ra[q] = 0;
+            } else {
+              ptx::tmem_ld_32x32b_x16(tcol(x), ra);
+              ptx::tmem_ld_wait();
+            }
             emit16(x, ra);
           }
           release_slot(j);

@@ -404,6 +404,24 @@ def sweep_swiglu(batches=(256, 1024, 2048), tps=(8, 1), hidden=4096, ffn=14336, 
                     if us < best.get(mode, (float("inf"),))[0]:
                         best[mode] = (us, {"policy": type(pol).__name__,
                                            "tile": f"256x{pw}/256x{cw or 256}"})
+                # few row tiles (B <= 1024): split-K slices to fill the CTA pairs, reduced on
+                # the tensor cores (the only split path under SwiGLU)
+                for (z1, z2), pol in itertools.product(
+                        ((2, 1), (4, 1), (4, 2), (8, 2)) if b <= 1024 else (), pols):
+                    pw = 512
+                    try:
+                        ch = SwigluChain(x, packed[pw], wd, policy=pol, mode=mode, tile_n=256,
+                                         cta_group=2, prod_tile_n=pw, cons_tile_n=512,
+                                         prod_splits=z1, cons_splits=z2,
+                                         extra_flags=REDUCE_TC)
+                    except Exception:  # K not divisible into the slices
+                        continue
+                    us = _time(ch, iters=20)
+                    _check_watchdog(ch, {"splits": (z1, z2), "policy": pol, "mode": mode})
+                    if us < best.get(mode, (float("inf"),))[0]:
+                        best[mode] = (us, {"policy": type(pol).__name__,
+                                           "tile": "256x512/256x512", "splits": [z1, z2],
+                                           "reduce": "tensor-core"})
 
             def torch_mlp():
                 return (torch.nn.functional.silu(x @ wg.t()) * (x @ wu.t())) @ wd.t()

@@ -11,7 +11,8 @@ w1 = (torch.randn(c, 3, 3, c, device="cuda") / (9 * c) ** 0.5).half()
 w2 = (torch.randn(c, 3, 3, c, device="cuda") / (9 * c) ** 0.5).half()
 for b in (128, 256):
     x = torch.randn(b, hw, hw, c, device="cuda").half()
-    for name, fl, mode in (("fused", 0, "fused"), ("stream", 0, "stream"), ("stream no-mma", 1 << 13, "stream"),
-                           ("fused no-wait", 1 << 12, "fused")):
+    for name, fl, mode in (("stream", 0, "stream"), ("stream no-mma", 1 << 13, "stream"),
+                           ("stream no-tmem-ld", 1 << 24, "stream"),
+                           ("stream no-mma no-tmem-ld", (1 << 13) | (1 << 24), "stream")):
         ch = ts.ConvChain(x, w1, w2, tile_n=64, cta_group=1, mode=mode, halo=True, extra_flags=fl)
         print(f"B={b} {name}: {planner._time(ch, iters=20):.1f} us", flush=True)

@@ -236,3 +236,32 @@ def test_vgg19_conv_pair(hw, c):
             check_close(ch.y, y_ref, torch.float16)
             if mode == "fused":
                 check_sync(ch.cs)
+
+
+@pytest.mark.parametrize("b,z1,z2,pol", [(256, 4, 2, ts.RowSync()), (256, 8, 2, ts.TileSync()),
+                                         (1024, 2, 1, ts.RowSync())])
+def test_llama_swiglu_split_tc_reduce(b, z1, z2, pol):
+    """LLaMA-8B SwiGLU TP=8 shard with split-K slices under the SwiGLU epilogue (the
+    tensor-core reduction: the owner's accumulator holds gate + up sums before SiLU(g)*u)."""
+    g = torch.Generator().manual_seed(b + z1)
+    hd, f = 4096, 14336 // 8
+    x = torch.randn(b, hd, generator=g).bfloat16()
+    wg = (torch.randn(f, hd, generator=g) / hd ** 0.5).bfloat16()
+    wu = (torch.randn(f, hd, generator=g) / hd ** 0.5).bfloat16()
+    wd = (torch.randn(hd, f, generator=g) / f ** 0.5).bfloat16()
+    ch = ts.SwigluChain(x.cuda(), ts.interleave_gate_up(wg, wu, 512).cuda(), wd.cuda(), policy=pol,
+                        tile_n=256, cta_group=2, prod_tile_n=512, cons_tile_n=512,
+                        prod_splits=z1, cons_splits=z2, extra_flags=planner.REDUCE_TC,
+                        keep_sems=True)
+    ch()
+    torch.cuda.synchronize()
+    assert not ch.cs.watchdog_fired()
+    _, y_ref = O.swiglu_chain(x.float().numpy(), wg.float().numpy(), wu.float().numpy(),
+                              wd.float().numpy(), "bf16")
+    check_close(ch.y, y_ref, torch.bfloat16)
+    stages = [{"id": s.id, "grid": (s.grid.x, s.grid.y, s.grid.z), "k_steps": s.k_steps,
+               "order": ("row_major", 1)} for s in ch.cs.scenario().stages]
+    deps = [{"producer": "gate_up", "consumer": "down", "operand": "a",
+             "policy": ("row" if isinstance(pol, ts.RowSync) else "tile", 0)}]
+    assert {k: tuple(v) for k, v in O.final_semaphores(stages, deps).items()} == \
+        ch.cs.final_semaphores()
