@@ -189,7 +189,7 @@ struct Cfg {
   // 256 x 256 tiles at 4 K-blocks = 2048 MMA cycles of buffering, too little to cover
   // loaded HBM latency: 31-51% of the MMA floor against cuBLAS's 97% on the same tile.)
 #ifndef TS_CHUNKS
-#define TS_CHUNKS 11
+#define TS_CHUNKS 12
 #endif
   static constexpr int kChunks = TS_CHUNKS;
   static constexpr int kTileM = SW ? BN : 128 * CG;  // activation rows of a tile
@@ -217,7 +217,11 @@ struct Cfg {
 #endif
   // chunked tiles: a 4-KB tf32 identity (the B operand of the split-K reduction MMAs,
   // 32 x 32 for one CTA, this CTA's 16 rows of it for a pair) after the staging blocks
-  static constexpr int kIdentOff = kStageOff + (kEpiThreads / 32) * TS_STAGE_WARP_BYTES;
+  // (chunked tiles: 2-KB blocks, half a warp's rows per pass, so that twelve ring chunks
+  // and the identity fit: the eleven-chunk ring of an earlier build cost ~2% on the
+  // 256 x 512 chains — three K-blocks in flight instead of four)
+  static constexpr int kStageWarpBytes = kChunked ? 2048 : TS_STAGE_WARP_BYTES;
+  static constexpr int kIdentOff = kStageOff + (kEpiThreads / 32) * kStageWarpBytes;
   static constexpr int kBarOffset = kChunked ? kIdentOff + 4096 : kStages * kStageBytes;
   // K-block full, commit-group empty; tmem full/empty x2; tile ring full/empty; peer_done
   // halo conv (hmode != 0, CG = 1, BN = 64): 9 weight taps (72 KB) then 2-4 window
@@ -1553,24 +1557,48 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
     // its row (32 words); they go to shared memory (16-B granules XOR-swizzled by row)
     // and come back as 4 rows x 128 B per instruction, written with 16-B stores to
     // dst(row_in_warp, granule) (nullptr = skip).
-    uint32_t* stg = reinterpret_cast<uint32_t*>(smem + C::kStageOff + (warp - 4) * 4096);
+    uint32_t* stg =
+        reinterpret_cast<uint32_t*>(smem + C::kStageOff + (warp - 4) * C::kStageWarpBytes);
     // split-K partial planes: written evict_last, read evict_first, so they stay in L2
     // between the slices instead of round-tripping through HBM under the weight streams
     // (diagnostic flag bit 26: no hints)
     auto stage_rows_hint = [&](const uint32_t (&v)[32], auto&& dst, uint64_t pol_el) {
+      if constexpr (C::kStageWarpBytes >= 4096) {
 #pragma unroll
-      for (int g = 0; g < 8; ++g)
-        *reinterpret_cast<uint4*>(stg + lane * 32 + ((g ^ (lane & 7)) * 4)) =
-            make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
-      __syncwarp();
+        for (int g = 0; g < 8; ++g)
+          *reinterpret_cast<uint4*>(stg + lane * 32 + ((g ^ (lane & 7)) * 4)) =
+              make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+        __syncwarp();
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int rr = 4 * i + (lane >> 3), g = lane & 7;
-        const uint4 q = *reinterpret_cast<const uint4*>(stg + rr * 32 + ((g ^ (rr & 7)) * 4));
-        uint4* d = dst(rr, g);
-        if (d != nullptr) ptx::st_global_v4_hint(d, q, pol_el);
+        for (int i = 0; i < 8; ++i) {
+          const int rr = 4 * i + (lane >> 3), g = lane & 7;
+          const uint4 q = *reinterpret_cast<const uint4*>(stg + rr * 32 + ((g ^ (rr & 7)) * 4));
+          uint4* d = dst(rr, g);
+          if (d != nullptr) ptx::st_global_v4_hint(d, q, pol_el);
+        }
+        __syncwarp();
+      } else {
+        // 2-KB block: rows [16 h, 16 h + 16) per pass
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if ((lane >> 4) == h) {
+            const int lr = lane & 15;
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+              *reinterpret_cast<uint4*>(stg + lr * 32 + ((g ^ (lr & 7)) * 4)) =
+                  make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = 4 * i + (lane >> 3), g = lane & 7;
+            const uint4 q = *reinterpret_cast<const uint4*>(stg + rr * 32 + ((g ^ (rr & 7)) * 4));
+            uint4* d = dst(16 * h + rr, g);
+            if (d != nullptr) ptx::st_global_v4_hint(d, q, pol_el);
+          }
+          __syncwarp();
+        }
       }
-      __syncwarp();
     };
     auto stage_rows = [&](const uint32_t (&v)[32], auto&& dst) {
       stage_rows_hint(v, dst, (p.flags >> 26) & 1 ? ptx::policy_evict_normal()

@@ -213,6 +213,13 @@ def pick_mlp(x, w1, w2, mode="fused", tie=0.015):
     # cap moves the SM clock between measurements): re-time the fastest four round-robin,
     # three rounds of 20 chains, and keep the best median.
     top = sorted(timed, key=lambda t: t[0])[:4]
+    # the fastest unsplit-GeMM1 candidate joins the re-timing: the preference below must
+    # compare re-timed medians, not one first-pass sample
+    lean0 = [(us, kw) for us, kw in sorted(timed, key=lambda t: t[0])
+             if kw.get("prod_splits", 1) == 1 and not kw.get("swap_ab", False)]
+    if x.shape[0] >= 512 and lean0 and all(kw is not lean0[0][1] for _, kw in top):
+        top.append(lean0[0])
+    retimed = set()
     if len(top) > 1:
         chains = [(kw, MlpChain(x, w1, w2, **kw)) for _, kw in top]
         runs = {id(kw): [] for kw, _ in chains}
@@ -225,10 +232,11 @@ def pick_mlp(x, w1, w2, mode="fused", tie=0.015):
         best_us, _, best = min(scored, key=lambda t: (t[0], t[1]))
         timed = [(statistics.median(runs[id(kw)]) if id(kw) in runs else us, kw)
                  for us, kw in timed]
+        retimed = set(runs)
     if x.shape[0] >= 512 and best is not None and best.get("prod_splits", 1) > 1:
         lean = [(us, kw) for us, kw in timed
                 if kw.get("prod_splits", 1) == 1 and not kw.get("swap_ab", False)
-                and us <= best_us * (1 + tie)]
+                and id(kw) in retimed and us <= best_us * (1 + tie)]
         if lean:
             best = min(lean, key=lambda t: t[0])[1]
     return best, table
