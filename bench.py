@@ -248,13 +248,20 @@ def main():
     w2 = (torch.randn(H, FFN, device=dev) / FFN ** 0.5).half()
     flops = 2 * b * H * FFN * 2
 
-    # co-scheduling choice (policy, tile order, CTA group) from measured candidates
+    # co-scheduling choice (policy, tile order, CTA group) from measured candidates; the
+    # fixed plan is the B=1024 configuration that led every A/B of round 2
+    # (profiles/r02ff_ready_first_and_ring.txt): GeMM1 in two split-K slices, GeMM2
+    # claimed in bands of four row tiles
+    fixed = dict(policy=ts.RowSync(), tile_n=256, cta_group=2, prod_tile_n=512,
+                 cons_tile_n=512, prod_splits=2, cons_order=ts.BandedColumnMajor(4))
     if args.plan == "auto":
         best, cands = planner.pick_mlp(x, w1, w2, mode="fused")
         base, bcands = planner.pick_mlp(x, w1, w2, mode="stream")
+        if b == 1024:
+            # guard against a noisy pick: the planner's choice and the fixed plan are
+            # re-timed round robin (3 x 20 chains each) and the faster median is kept
+            best = planner.pick_between(x, w1, w2, [best, dict(fixed, mode="fused")])
     else:
-        fixed = dict(policy=ts.RowSync(), tile_n=256, cta_group=2, prod_tile_n=512,
-                     cons_tile_n=512, cons_tail=(22, 2), cons_order=ts.BandedColumnMajor(4))
         best, cands = dict(fixed, mode="fused"), []
         base, bcands = dict(fixed, mode="stream"), []
     chain = ts.MlpChain(x, w1, w2, **best)

@@ -242,6 +242,20 @@ def pick_mlp(x, w1, w2, mode="fused", tie=0.015):
     return best, table
 
 
+def pick_between(x, w1, w2, plans, rounds=3, iters=20):
+    """The plan (MlpChain kwargs) with the lowest median over `rounds` round-robin timings
+    of `iters` chains each (ties: the first listed)."""
+    chains = [MlpChain(x, w1, w2, **kw) for kw in plans]
+    runs = [[] for _ in plans]
+    for _ in range(rounds):
+        for i, ch in enumerate(chains):
+            runs[i].append(_time(ch, iters=iters, warm=3))
+    for kw, ch in zip(plans, chains):
+        _check_watchdog(ch, kw)
+    med = [statistics.median(r) for r in runs]
+    return plans[min(range(len(plans)), key=lambda i: (med[i], i))]
+
+
 def sweep_mlp(batches=(1, 64, 256, 512, 1024, 2048), hidden=12288, ffn=6144, device=None):
     """GPT-3 MLP shard latency per batch: best fused, best stream-synced, cuBLAS."""
     torch.manual_seed(7)
