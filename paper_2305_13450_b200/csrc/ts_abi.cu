@@ -554,11 +554,25 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
           sp.hmode = 1;
           sp.hs = srow;
           sp.hrpt = 128 / srow < st.conv_h ? 128 / srow : st.conv_h;
+          sp.hsub = 1;
+          // two 128-position sub-tiles per item (rows that fit 256 positions) when their
+          // window still fits two buffers and the layer still has two items per SM: one
+          // claim, window, commit and accumulator hand-off per two tiles (the per-item
+          // pipeline cost dominates 128 x 64 tiles; B=256 56x56x64: 325 -> 248 us)
+          const int rpt2 = 256 / srow < st.conv_h ? 256 / srow : st.conv_h;
+          if (rpt2 * srow > 128 &&
+              (196608 - 9 * 8192) / (((rpt2 + 2) * srow * 128 + 1023) / 1024 * 1024) >= 2 &&
+              static_cast<long long>(st.conv_n) * ((st.conv_h + rpt2 - 1) / rpt2) >=
+                  2LL * sm_count()) {
+            sp.hrpt = rpt2;
+            sp.hsub = 2;
+          }
           sp.hrows = sp.hrpt + 2;
           sp.htpi = (st.conv_h + sp.hrpt - 1) / sp.hrpt;
           sp.htpr = 0;
         } else {
           sp.hmode = 2;
+          sp.hsub = 1;
           sp.hs = 130;
           sp.hrows = 3;
           sp.hrpt = 1;

@@ -123,6 +123,7 @@ struct StageParams {
   // (row stride hs = W + 2, two junk columns per row); 2: a tile = 128 positions of one row
   // (hs = 130). 0: the im2col-per-tap path.
   int hmode, hs, htpi, htpr, hrows, hbytes;
+  int hsub;  // 128-position sub-tiles per item (hmode 1: 2 when 256 positions' window fits)
   int hrpt;      // rows mode: image rows per tile (a tile = hrpt x hs positions)
   int hnb, hwin;  // window buffers in flight and their stride (bytes, 1024-aligned)
   CUtensorMap tmap_win;  // (C, W, H, N) box (64, hs, hrows, 1), 128-B swizzle
@@ -205,7 +206,9 @@ struct Cfg {
   // accumulates into the same TMEM region; rotating over kAcc independent accumulators
   // (summed in the epilogue) keeps the tensor pipe busy.
   static constexpr int kAcc = SW ? (BN >= 256 ? 1 : 256 / BN > 8 ? 8 : 256 / BN) : 1;
-  static constexpr int kAccCols = kAcc * BN;           // TMEM columns of one tile buffer
+  // (single-CTA 64-wide kernels: 128 columns, room for a halo-conv item's two sub-tiles)
+  static constexpr int kAccCols =
+      kAcc * BN * ((!kChunked && CG == 1 && !SW && BN == 64) ? 2 : 1);  // TMEM cols per buffer
   static constexpr int kTmemCols = 2 * kAccCols;       // two tile buffers
   static constexpr int kRing = kChunked ? kChunks : kStages;  // ring entries
   // chunked tiles: a 4-KB per-warp staging block after the ring turns the epilogue's
@@ -1396,14 +1399,28 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
                 trace_event(p, ptx::global_timer(), 5, t5.s, t5.tb, -1, -1, -1, -1, t5.tx, t5.ty);
               }
               const uint32_t wb = ptx::smem_u32(smem + 9 * 8192 + b * sp.hwin);
+              if (sp.hsub > 1) {
+                // two sub-tiles: window rows 128 + ... into accumulator columns [64, 128)
 #pragma unroll 1
-              for (int tap = 0; tap < 9; ++tap) {
-                const int r = tap / 3, s = tap - 3 * (tap / 3);
-                const uint64_t ad = ptx::smem_desc_k_sw128(wb + (ht.base + r * sp.hs + s) * 128);
-                const uint64_t bdd = ptx::smem_desc_k_sw128(ptx::smem_u32(smem + tap * 8192));
-                // (one accumulator: a second one for alternating taps measured no faster and
-                // doubles the epilogue's TMEM reads, the other pacing resource)
-                if (!no_mma) ptx::umma_f16_kblock<CG>(d_tmem, ad, bdd, kIdesc, tap != 0);
+                for (int tap = 0; tap < 9; ++tap) {
+                  const int r = tap / 3, s = tap - 3 * (tap / 3);
+                  const uint64_t ad = ptx::smem_desc_k_sw128(wb + (ht.base + r * sp.hs + s) * 128);
+                  const uint64_t bdd = ptx::smem_desc_k_sw128(ptx::smem_u32(smem + tap * 8192));
+                  if (!no_mma) {
+                    ptx::umma_f16_kblock<CG>(d_tmem, ad, bdd, kIdesc, tap != 0);
+                    ptx::umma_f16_kblock<CG>(d_tmem + 64, ad + 1024, bdd, kIdesc, tap != 0);
+                  }
+                }
+              } else {
+#pragma unroll 1
+                for (int tap = 0; tap < 9; ++tap) {
+                  const int r = tap / 3, s = tap - 3 * (tap / 3);
+                  const uint64_t ad = ptx::smem_desc_k_sw128(wb + (ht.base + r * sp.hs + s) * 128);
+                  const uint64_t bdd = ptx::smem_desc_k_sw128(ptx::smem_u32(smem + tap * 8192));
+                  // (one accumulator: a second one for alternating taps measured no faster
+                  // and doubles the epilogue's TMEM reads, the other pacing resource)
+                  if (!no_mma) ptx::umma_f16_kblock<CG>(d_tmem, ad, bdd, kIdesc, tap != 0);
+                }
               }
               ptx::umma_commit(&win_empty[b]);
             }
@@ -2255,6 +2272,23 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
               ptx::tmem_ld_wait();
             }
             emit16(x, ra);
+          }
+          if constexpr (C::kHaloOk) {
+            if (st.hmode && st.hsub > 1) {
+              // a halo-conv item's second sub-tile: item rows 128 + ..., accumulator
+              // columns [64, 128) of the same buffer
+              const int px = halo_pixel(st, halo_tile(st, t.tx), 128 + ew * 32 + lane);
+              row_ok = px >= 0;
+              out = reinterpret_cast<T*>(st.c) + static_cast<size_t>(px < 0 ? 0 : px) * st.ldc +
+                    col0;
+#pragma unroll 1
+              for (int x = lo; x < hi; x += 16) {
+                uint32_t ra[16];
+                ptx::tmem_ld_32x32b_x16(t_lane + 64 + x, ra);
+                ptx::tmem_ld_wait();
+                emit16(x, ra);
+              }
+            }
           }
           release_slot(j);
         }

@@ -110,7 +110,8 @@ class CuStage:
         positions separately (``halo_tiles_per_image``)."""
         if self.kind == "conv" and self.cs.conv_halo:
             n, h, w = self.conv
-            return Dim3(n * halo_tiles_per_image(h, w), max(1, self.n // self.width), self.splits)
+            return Dim3(n * halo_tiles_per_image(h, w, n, _device_sms()),
+                        max(1, self.n // self.width), self.splits)
         return Dim3(-(-self.m // self.cs.tile_m), max(1, self.n // self.width), self.splits)
 
     def flops(self) -> int:
@@ -124,13 +125,34 @@ class CuStage:
         return self
 
 
-def halo_tiles_per_image(h: int, w: int) -> int:
-    """Tiles of one H x W image under TS_FLAG_CONV_HALO (ts_abi.cu build_params): the whole
-    width-padded rows (row stride W + 2) that fit 128 positions while W + 2 <= 128, else
+_SMS: int | None = None
+
+
+def _device_sms() -> int:
+    """SM count of the current device, as the library sees it (ts_device_sm_count)."""
+    global _SMS
+    if _SMS is None:
+        out = ctypes.c_int(0)
+        _lib.check(_lib.load().ts_device_sm_count(ctypes.byref(out)))
+        _SMS = out.value
+    return _SMS
+
+
+def halo_tiles_per_image(h: int, w: int, n: int = 1, sms: int = 148) -> int:
+    """Tiles (items) of one H x W image under TS_FLAG_CONV_HALO (ts_abi.cu build_params):
+    the whole width-padded rows (row stride W + 2) that fit 256 positions — two 128-row
+    sub-tiles — when their window fits two buffers and n images give two items per SM
+    (`sms`: the device's SM count), else 128 positions, while W + 2 <= 128; else
     128-position segments of each row."""
     srow = w + 2
     if srow <= 128:
         rpt = min(128 // srow, h)
+        # two 128-position sub-tiles per item when their window fits two buffers and the
+        # n images still give two items per SM
+        rpt2 = min(256 // srow, h)
+        win2 = -(-((rpt2 + 2) * srow * 128) // 1024) * 1024
+        if rpt2 * srow > 128 and (196608 - 9 * 8192) // win2 >= 2 and n * -(-h // rpt2) >= 2 * sms:
+            rpt = rpt2
         return -(-h // rpt)
     return h * -(-w // 128)
 

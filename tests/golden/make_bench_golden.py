@@ -131,7 +131,7 @@ def main() -> None:
             gx = -(-(b * hw * hw) // tm)
             if kw.get("halo"):  # halo-staged tiles: per-image re-tiling
                 from paper_2305_13450_b200.cusync import halo_tiles_per_image
-                gx = b * halo_tiles_per_image(hw, hw)
+                gx = b * halo_tiles_per_image(hw, hw, b, 148)  # B200: 148 SMs
             z = kw["prod_splits"]
             g = (gx, c // kw["tile_n"], z)
             add(f"{net}_conv_{hw}x{c}_b{b}", [("conv1", g, 9 * c // kw["tile_n"], rm),

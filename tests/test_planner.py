@@ -44,3 +44,19 @@ def test_wave_table_matches_survey_appendix_b():
     t = planner.wave_table(1024, 6144, 12288, 128, 256)
     assert t["tiles"] == (192, 384)
     assert t["stream_waves"] == 5 and t["fine_waves"] == 4
+
+
+@pytest.mark.parametrize("h,w,n,want", [
+    (56, 56, 1, 28),     # two 58-wide padded rows per 128-position tile
+    (56, 56, 16, 28),    # 16 x 14 = 224 two-sub-tile items < 2 x 148: stay at 128
+    (56, 56, 32, 14),    # four rows (232 of 256 positions) per two-sub-tile item
+    (28, 28, 80, 4),     # eight 30-wide rows per item
+    (28, 28, 8, 7),
+    (14, 14, 300, 1),    # the whole 16-wide padded image in one item
+    (7, 7, 1000, 1),     # 63 positions: one sub-tile is enough
+    (224, 224, 64, 224 * 2),  # wide rows: 128-position row segments
+])
+def test_halo_tiles_per_image(h, w, n, want):
+    """Mirror of the halo-conv re-tiling in ts_abi.cu build_params (host logic)."""
+    from paper_2305_13450_b200.cusync import halo_tiles_per_image
+    assert halo_tiles_per_image(h, w, n, 148) == want
