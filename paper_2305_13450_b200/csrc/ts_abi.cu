@@ -549,6 +549,9 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
           return fail(TS_ERR_CONFIG, "stage %d: halo-staged convolution needs Cin = Cout = 64, "
                       "cta_group 1, tile_n 64, no split-K, width <= 254", s);
         const int srow = st.conv_w + 2;
+        // window space of the BN = 64 kernel: its 9 x 24 KB operand ring minus the resident
+        // weight taps (9 x 8 KB)
+        constexpr int kHaloWindowBytes = 9 * 24576 - 9 * 8192;
         if (srow <= 128) {
           // rows mode: a tile = the whole width-padded rows that fit 128 positions
           sp.hmode = 1;
@@ -561,7 +564,7 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
           // pipeline cost dominates 128 x 64 tiles; B=256 56x56x64: 325 -> 248 us)
           const int rpt2 = 256 / srow < st.conv_h ? 256 / srow : st.conv_h;
           if (rpt2 * srow > 128 &&
-              (196608 - 9 * 8192) / (((rpt2 + 2) * srow * 128 + 1023) / 1024 * 1024) >= 2 &&
+              kHaloWindowBytes / (((rpt2 + 2) * srow * 128 + 1023) / 1024 * 1024) >= 2 &&
               static_cast<long long>(st.conv_n) * ((st.conv_h + rpt2 - 1) / rpt2) >=
                   2LL * sm_count()) {
             sp.hrpt = rpt2;
@@ -577,11 +580,20 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
           sp.hrows = 3;
           sp.hrpt = 1;
           sp.htpr = (st.conv_w + 127) / 128;
-          sp.htpi = st.conv_h * sp.htpr;
+          // two image rows of the segment per item (a 4-row window) when two such windows
+          // fit and the layer keeps two items per SM
+          if (st.conv_h >= 2 && kHaloWindowBytes / ((4 * 130 * 128 + 1023) / 1024 * 1024) >= 2 &&
+              static_cast<long long>(st.conv_n) * ((st.conv_h + 1) / 2) * sp.htpr >=
+                  2LL * sm_count()) {
+            sp.hrpt = 2;
+            sp.hrows = 4;
+            sp.hsub = 2;
+          }
+          sp.htpi = (st.conv_h + sp.hrpt - 1) / sp.hrpt * sp.htpr;
         }
         sp.hbytes = sp.hrows * sp.hs * 128;
         sp.hwin = (sp.hbytes + 1023) / 1024 * 1024;
-        sp.hnb = (196608 - 9 * 8192) / sp.hwin;  // the BN = 64 kernel's operand ring
+        sp.hnb = kHaloWindowBytes / sp.hwin;  // the BN = 64 kernel's operand ring
         if (sp.hnb > 4) sp.hnb = 4;
         if (sp.hnb < 2)
           return fail(TS_ERR_CONFIG, "stage %d: conv window of %d bytes too large", s, sp.hbytes);

@@ -199,8 +199,11 @@ struct Cfg {
   static constexpr int kABytes = 128 * kBK * 2;      // UMMA-M operand stage
   static constexpr int kBBytes = kBRows * kBK * 2;   // UMMA-N operand stage
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
-  static constexpr int kStagesMax = SW ? 12 : 8;
+  // (single-CTA 64-wide kernels: 9 x 24 KB, so a halo-conv layer's windows get 144 KB next
+  // to its 72 KB of resident weights)
+  static constexpr bool kNarrow1 = !SW && CG == 1 && BN == 64;
+  static constexpr int kStagesRaw = ((kNarrow1 ? 216 : 200) * 1024) / kStageBytes;
+  static constexpr int kStagesMax = SW ? 12 : (kNarrow1 ? 9 : 8);
   static constexpr int kStages = kStagesRaw > kStagesMax ? kStagesMax : kStagesRaw;
   // Narrow swapped MMAs (128 x BN x 16, BN <= 64) are latency-bound when every one
   // accumulates into the same TMEM region; rotating over kAcc independent accumulators
@@ -692,8 +695,9 @@ __device__ __forceinline__ HaloTile halo_tile(const StageParams& st, int tx) {
     h.w0 = 0;
     h.base = 0;
   } else {
-    h.h0 = lt / st.htpr;
-    h.w0 = (lt - h.h0 * st.htpr) * 128;
+    const int rt = lt / st.htpr;  // row group (hrpt image rows) of the tile
+    h.h0 = rt * st.hrpt;
+    h.w0 = (lt - rt * st.htpr) * 128;
     h.base = 0;
   }
   return h;
@@ -708,8 +712,9 @@ __device__ __forceinline__ int halo_pixel(const StageParams& st, const HaloTile&
     h = ht.h0 + m / st.hs;
     w = m % st.hs;
   } else {
-    h = ht.h0;
-    w = ht.w0 + m;
+    // sub-tile m / 128 = image row h0 + m / 128 of the segment
+    h = ht.h0 + (m >> 7);
+    w = ht.w0 + (m & 127);
   }
   if (h >= st.conv_h || w >= st.conv_w) return -1;
   return (ht.n * st.conv_h + h) * st.conv_w + w;
@@ -1051,11 +1056,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
                 const int hhi = hhi0 < st.conv_h - 1 ? hhi0 : st.conv_h - 1;
                 for (int u = hlo / st.hrpt; u <= hhi / st.hrpt; ++u) wait_tile(base_t + u);
               } else {
-                const int hhi = ht.h0 + 1 < st.conv_h - 1 ? ht.h0 + 1 : st.conv_h - 1;
+                const int hhi0 = ht.h0 + st.hrpt;  // last input row the window reads
+                const int hhi = hhi0 < st.conv_h - 1 ? hhi0 : st.conv_h - 1;
                 const int s0 = ht.w0 > 0 ? (ht.w0 - 1) / 128 : 0;
                 const int s1 = (ht.w0 + 128 < st.conv_w - 1 ? ht.w0 + 128 : st.conv_w - 1) / 128;
-                for (int hh = hlo; hh <= hhi; ++hh)
-                  for (int sg = s0; sg <= s1; ++sg) wait_tile(base_t + hh * st.htpr + sg);
+                for (int rg = hlo / st.hrpt; rg <= hhi / st.hrpt; ++rg)
+                  for (int sg = s0; sg <= s1; ++sg) wait_tile(base_t + rg * st.htpr + sg);
               }
               if (uleader)
                 trace_event(p, ptx::global_timer(), 2, t.s, t.tb, 0, d, t.tx, dp.pgz, t.tx, t.ty, t.tz);
@@ -1400,7 +1406,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
               }
               const uint32_t wb = ptx::smem_u32(smem + 9 * 8192 + b * sp.hwin);
               if (sp.hsub > 1) {
-                // two sub-tiles: window rows 128 + ... into accumulator columns [64, 128)
+                // two sub-tiles into accumulator columns [64, 128): the window rows 128 + ...
+                // (rows mode) or one image row further (segment mode), in 16-B units
+                const uint64_t sub_off = (sp.hmode == 1 ? 128 : sp.hs) * 8;
 #pragma unroll 1
                 for (int tap = 0; tap < 9; ++tap) {
                   const int r = tap / 3, s = tap - 3 * (tap / 3);
@@ -1408,7 +1416,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
                   const uint64_t bdd = ptx::smem_desc_k_sw128(ptx::smem_u32(smem + tap * 8192));
                   if (!no_mma) {
                     ptx::umma_f16_kblock<CG>(d_tmem, ad, bdd, kIdesc, tap != 0);
-                    ptx::umma_f16_kblock<CG>(d_tmem + 64, ad + 1024, bdd, kIdesc, tap != 0);
+                    ptx::umma_f16_kblock<CG>(d_tmem + 64, ad + sub_off, bdd, kIdesc, tap != 0);
                   }
                 }
               } else {

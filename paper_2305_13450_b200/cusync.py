@@ -138,12 +138,15 @@ def _device_sms() -> int:
     return _SMS
 
 
+_HALO_WINDOW_BYTES = 9 * 24576 - 9 * 8192  # ts_abi.cu: the BN = 64 ring minus resident weights
+
+
 def halo_tiles_per_image(h: int, w: int, n: int = 1, sms: int = 148) -> int:
     """Tiles (items) of one H x W image under TS_FLAG_CONV_HALO (ts_abi.cu build_params):
     the whole width-padded rows (row stride W + 2) that fit 256 positions — two 128-row
     sub-tiles — when their window fits two buffers and n images give two items per SM
     (`sms`: the device's SM count), else 128 positions, while W + 2 <= 128; else
-    128-position segments of each row."""
+    128-position segments of one row, or of two rows under the same conditions."""
     srow = w + 2
     if srow <= 128:
         rpt = min(128 // srow, h)
@@ -151,10 +154,14 @@ def halo_tiles_per_image(h: int, w: int, n: int = 1, sms: int = 148) -> int:
         # n images still give two items per SM
         rpt2 = min(256 // srow, h)
         win2 = -(-((rpt2 + 2) * srow * 128) // 1024) * 1024
-        if rpt2 * srow > 128 and (196608 - 9 * 8192) // win2 >= 2 and n * -(-h // rpt2) >= 2 * sms:
+        if rpt2 * srow > 128 and _HALO_WINDOW_BYTES // win2 >= 2 and n * -(-h // rpt2) >= 2 * sms:
             rpt = rpt2
         return -(-h // rpt)
-    return h * -(-w // 128)
+    segs = -(-w // 128)
+    # two image rows of a segment per item when two 4-row windows fit
+    win2 = -(-(4 * 130 * 128) // 1024) * 1024
+    rows = 2 if h >= 2 and _HALO_WINDOW_BYTES // win2 >= 2 and n * -(-h // 2) * segs >= 2 * sms else 1
+    return -(-h // rows) * segs
 
 
 @dataclass

@@ -17,9 +17,10 @@ from test_gpu_chain import _scenario_dicts, check_close
 pytestmark = pytest.mark.gpu
 
 # (32, 56) and (80, 28): items of two 128-position sub-tiles (enough images for two items
-# per SM); the rest one sub-tile
+# per SM); (2, 224) and (5, 129): wide images, two rows of a segment per item (129: an odd
+# height, the last item holds one row); the rest one sub-tile
 CASES = [(1, 56), (2, 56), (8, 56), (3, 28), (4, 14), (5, 7), (1, 224), (2, 130), (32, 56),
-         (80, 28)]
+         (80, 28), (2, 224), (5, 129)]
 
 
 def make(b, hw, c=64, seed=0):

@@ -54,7 +54,8 @@ def test_wave_table_matches_survey_appendix_b():
     (28, 28, 8, 7),
     (14, 14, 300, 1),    # the whole 16-wide padded image in one item
     (7, 7, 1000, 1),     # 63 positions: one sub-tile is enough
-    (224, 224, 64, 224 * 2),  # wide rows: 128-position row segments
+    (224, 224, 64, 224),  # wide rows: 128-position segments of two rows
+    (224, 224, 1, 448),   # one row per item: 224 two-row items would be < 2 per SM
 ])
 def test_halo_tiles_per_image(h, w, n, want):
     """Mirror of the halo-conv re-tiling in ts_abi.cu build_params (host logic)."""
