@@ -297,16 +297,26 @@ def sweep_attention(seqs=(512, 1024, 2048), hidden=12288, heads=12, device=None)
         x = torch.randn(s, hidden, device=device).half()
         best = {}
         for mode in ("fused", "stream"):
+            timed = []
             for cg, z, ow in itertools.product((1, 2), (1, 2, 4), (0, 512)):
                 if ow and cg == 1:
                     continue  # double-width output tiles are CTA-pair tiles
                 for pol in ([RowSync(), TileSync()] if mode == "fused" else [TileSync()]):
-                    ch = AttentionChain(x, wqkv, w2, second_policy=pol, mode=mode, cta_group=cg,
-                                        qkv_splits=z, out_tile_n=ow)
-                    us = _time(ch, iters=20)
-                    if us < best.get(mode, (float("inf"),))[0]:
-                        best[mode] = (us, {"cta_group": cg, "policy": type(pol).__name__,
-                                           "qkv_splits": z, "out_tile_n": ow or 256})
+                    kw = dict(second_policy=pol, mode=mode, cta_group=cg, qkv_splits=z,
+                              out_tile_n=ow)
+                    ch = AttentionChain(x, wqkv, w2, **kw)
+                    timed.append((_time(ch, iters=20), kw))
+            # the fastest three re-timed round robin (3 x 20 chains), best median kept
+            top = sorted(timed, key=lambda t: t[0])[:3]
+            chains = [AttentionChain(x, wqkv, w2, **kw) for _, kw in top]
+            runs = [[_time(ch, iters=20, warm=3) for ch in chains] for _ in range(3)]
+            med = [statistics.median(r[i] for r in runs) for i in range(len(chains))]
+            i = min(range(len(chains)), key=lambda j: med[j])
+            kw = top[i][1]
+            best[mode] = (med[i], {"cta_group": kw["cta_group"],
+                                   "policy": type(kw["second_policy"]).__name__,
+                                   "qkv_splits": kw["qkv_splits"],
+                                   "out_tile_n": kw["out_tile_n"] or 256})
         cu = _time(lambda: _torch_attention(x, wqkv, w2, heads), iters=20)
         flops = 2 * s * hidden * 3 * heads * 128 + 2 * s * heads * 128 * hidden
         rows.append({"seq": s, "fused_us": best["fused"][0], "stream_us": best["stream"][0],
