@@ -1399,12 +1399,18 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
             ptx::mbar_wait(&win_full[b], (hm / sp.hnb) & 1);
             ptx::tc_fence_after();
             if (lane == 0) {
-              const HaloTile ht = halo_tile(sp, decode(p, g).tx);
+              // (a tile's window always starts at its base pixel: halo_tile's base is 0, so
+              // the MMA warp needs no tile decode — integer divisions by runtime grid sizes
+              // in the single issuing thread, on the per-item critical path)
               if (tr) {
                 const Tile t5 = decode(p, g);
                 trace_event(p, ptx::global_timer(), 5, t5.s, t5.tb, -1, -1, -1, -1, t5.tx, t5.ty);
               }
-              const uint32_t wb = ptx::smem_u32(smem + 9 * 8192 + b * sp.hwin);
+              // tap (r, s): A = the window from row r * hs + s (16-B descriptor units: 8 per
+              // 128-B row), B = tap weights (8 KB = 512 units apart)
+              const uint64_t ad0 = ptx::smem_desc_k_sw128(ptx::smem_u32(smem + 9 * 8192 + b * sp.hwin));
+              const uint64_t bd0 = ptx::smem_desc_k_sw128(ptx::smem_u32(smem));
+              const int hs8 = sp.hs * 8;
               if (sp.hsub > 1) {
                 // two sub-tiles into accumulator columns [64, 128): the window rows 128 + ...
                 // (rows mode) or one image row further (segment mode), in 16-B units
@@ -1412,8 +1418,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
 #pragma unroll 1
                 for (int tap = 0; tap < 9; ++tap) {
                   const int r = tap / 3, s = tap - 3 * (tap / 3);
-                  const uint64_t ad = ptx::smem_desc_k_sw128(wb + (ht.base + r * sp.hs + s) * 128);
-                  const uint64_t bdd = ptx::smem_desc_k_sw128(ptx::smem_u32(smem + tap * 8192));
+                  const uint64_t ad = ad0 + static_cast<uint64_t>(r * hs8 + s * 8);
+                  const uint64_t bdd = bd0 + static_cast<uint64_t>(tap * 512);
                   if (!no_mma) {
                     ptx::umma_f16_kblock<CG>(d_tmem, ad, bdd, kIdesc, tap != 0);
                     ptx::umma_f16_kblock<CG>(d_tmem + 64, ad + sub_off, bdd, kIdesc, tap != 0);
@@ -1423,8 +1429,8 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
 #pragma unroll 1
                 for (int tap = 0; tap < 9; ++tap) {
                   const int r = tap / 3, s = tap - 3 * (tap / 3);
-                  const uint64_t ad = ptx::smem_desc_k_sw128(wb + (ht.base + r * sp.hs + s) * 128);
-                  const uint64_t bdd = ptx::smem_desc_k_sw128(ptx::smem_u32(smem + tap * 8192));
+                  const uint64_t ad = ad0 + static_cast<uint64_t>(r * hs8 + s * 8);
+                  const uint64_t bdd = bd0 + static_cast<uint64_t>(tap * 512);
                   // (one accumulator: a second one for alternating taps measured no faster
                   // and doubles the epilogue's TMEM reads, the other pacing resource)
                   if (!no_mma) ptx::umma_f16_kblock<CG>(d_tmem, ad, bdd, kIdesc, tap != 0);
