@@ -362,7 +362,10 @@ int build_params(const ts_chain_desc* d, ts::ChainParams* p, bool with_tmaps) {
   p->ctl = d->scratch;
   p->coresident = 0;
   p->balanced = (d->flags & TS_FLAG_BALANCED) ? 1 : 0;
-  p->claim_batch = (d->flags & TS_FLAG_CONV_HALO) ? 2 : 1;
+  // one item per claim: batching halo-conv claims (2 / 4 / 8 per atomic) measured 1-95%
+  // slower once items carry two sub-tiles — the claim is not the per-item cost, the tail
+  // balance is (profiles/r02y_conv_halo.txt, r02pp)
+  p->claim_batch = 1;
   p->trace = static_cast<ts_trace_rec*>(d->trace);
   p->trace_cap = d->trace ? d->trace_cap : 0;
   const int dtype = d->stages[0].dtype;

@@ -152,7 +152,7 @@ struct ChainParams {
   int* ctl;
   int coresident;
   int balanced;   // TS_FLAG_BALANCED: static stream-K assignment (0 = dynamic claims)
-  int claim_batch;  // items per claim (halo-conv kernels: short tiles, one atomic per 2-4)
+  int claim_batch;  // items per claim (> 1: one atomic per claim_batch items; set to 1)
   ts_trace_rec* trace;
   int trace_cap;
   int flags;
