@@ -1359,11 +1359,55 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       const int group = commit_group(p.flags);
       uint32_t u = 0;  // TMEM accumulator-slot uses (a double-width tile takes two)
       int hm = 0, mw_stage = -1, mw_count = 0;  // halo conv: windows, resident-weight loads
+      // halo conv fast path: the current halo stage's item range and constants in registers
+      // (set by the general path below; measured ~2.9k cycles per item of parameter-block
+      // reads and bookkeeping in the issuing warp otherwise, profiles/r02y_conv_halo.txt)
+      int hc_lo = 0, hc_hi = 0, hc_hnb = 1, hc_hwin = 0, hc_hs8 = 0, hc_hsub = 1;
+      uint64_t hc_sub = 0;
 #pragma unroll 1
       for (int it = 0;; ++it) {
         int kbr;
         const int g = ring_take(it, QD && !uleader, kbr);
         if (g < 0) break;
+        if constexpr (C::kHaloOk) {
+          if (g >= hc_lo && g < hc_hi) {
+            ptx::mbar_wait(&tmem_empty[u & 1], ((u >> 1) & 1) ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + (u & 1) * C::kAccCols;
+            const int hq = hm / hc_hnb, b = hm - hq * hc_hnb;
+            ptx::mbar_wait(&win_full[b], hq & 1);
+            ptx::tc_fence_after();
+            if (lane == 0) {
+              const uint64_t ad0 =
+                  ptx::smem_desc_k_sw128(ptx::smem_u32(smem + 9 * 8192 + b * hc_hwin));
+              const uint64_t bd0 = ptx::smem_desc_k_sw128(ptx::smem_u32(smem));
+              if (hc_hsub > 1) {
+#pragma unroll 1
+                for (int tap = 0; tap < 9; ++tap) {
+                  const int r = tap / 3, s = tap - 3 * (tap / 3);
+                  const uint64_t ad = ad0 + static_cast<uint64_t>(r * hc_hs8 + s * 8);
+                  const uint64_t bdd = bd0 + static_cast<uint64_t>(tap * 512);
+                  ptx::umma_f16_kblock<CG>(d_tmem, ad, bdd, kIdesc, tap != 0);
+                  ptx::umma_f16_kblock<CG>(d_tmem + 64, ad + hc_sub, bdd, kIdesc, tap != 0);
+                }
+              } else {
+#pragma unroll 1
+                for (int tap = 0; tap < 9; ++tap) {
+                  const int r = tap / 3, s = tap - 3 * (tap / 3);
+                  const uint64_t ad = ad0 + static_cast<uint64_t>(r * hc_hs8 + s * 8);
+                  const uint64_t bdd = bd0 + static_cast<uint64_t>(tap * 512);
+                  ptx::umma_f16_kblock<CG>(d_tmem, ad, bdd, kIdesc, tap != 0);
+                }
+              }
+              ptx::umma_commit(&win_empty[b]);
+              ptx::umma_commit(&tmem_full[u & 1]);
+            }
+            ++hm;
+            __syncwarp();
+            u += 1;
+            continue;
+          }
+        }
         const StageParams& sp = p.st[stage_of(p, g)];
         if (sp.kind == kStageDot || sp.kind == kStageAllReduce)
           continue;  // no MMA, no accumulator buffer
@@ -1398,6 +1442,15 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
             const int b = hm % sp.hnb;
             ptx::mbar_wait(&win_full[b], (hm / sp.hnb) & 1);
             ptx::tc_fence_after();
+            if (!tr && !no_mma) {  // later items of this stage take the fast path above
+              hc_lo = sp.item_begin;
+              hc_hi = sp.item_end;
+              hc_hnb = sp.hnb;
+              hc_hwin = sp.hwin;
+              hc_hs8 = sp.hs * 8;
+              hc_hsub = sp.hsub;
+              hc_sub = static_cast<uint64_t>((sp.hmode == 1 ? 128 : sp.hs) * 8);
+            }
             if (lane == 0) {
               // (a tile's window always starts at its base pixel: halo_tile's base is 0, so
               // the MMA warp needs no tile decode — integer divisions by runtime grid sizes
