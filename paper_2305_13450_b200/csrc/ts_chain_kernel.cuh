@@ -37,7 +37,8 @@
 namespace ts {
 
 constexpr int kBK = 64;         // K elements per smem stage = one 128-B swizzle row
-constexpr int kTileRing = 4;    // tile-id hand-off ring between scheduler and consumers
+constexpr int kTileRing = 4;
+constexpr int kPostRing = 4;  // single-CTA kernels: posts handed to the post warp (warp 3)    // tile-id hand-off ring between scheduler and consumers
 // Operand pipeline barriers are indexed by K-block sequence number (full: TMA bytes
 // landed) and by commit group (empty: the MMAs that read a group of K-blocks are done),
 // not by smem ring entry. One tcgen05.commit then frees several K-blocks (measured: each
@@ -236,11 +237,12 @@ struct Cfg {
   static constexpr bool kHaloOk = !kChunked && CG == 1 && !SW && BN == 64 &&
                                   9 * 8192 + 2 * 50176 <= kHaloRegion;
   static constexpr int kNumBars =
-      kFullRing + kCommitRing + 4 + 2 * kTileRing + kPeerRing + 2 + 9;
+      kFullRing + kCommitRing + 4 + 2 * kTileRing + kPeerRing + 2 + 9 + 2 * kPostRing;
   // + tile ring ids, TMEM slot, flags and the last-arriver dot list (64 ints), ring-entry
   // owners (commit group that last read each entry)
   static constexpr int kSmemBytes =
-      1024 + kBarOffset + kNumBars * 8 + 64 + 272 + 4 * kRing + 4 * kTileRing + 16;
+      1024 + kBarOffset + kNumBars * 8 + 64 + 272 + 4 * kRing + 4 * kTileRing + 16 +
+      4 * kPostRing;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
   static_assert(kBRows % 8 == 0 && kBRows <= 256, "B box rows");
 };
@@ -795,7 +797,9 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
   uint64_t* hw_full = dot_done + 1;
   uint64_t* win_full = hw_full + 1;    // [4]
   uint64_t* win_empty = win_full + 4;  // [4]
-  int* ti_item = reinterpret_cast<int*>(win_empty + 4);
+  uint64_t* post_full = win_empty + 4;           // [kPostRing]: a post request is queued
+  uint64_t* post_empty = post_full + kPostRing;  // [kPostRing]: the post warp took it
+  int* ti_item = reinterpret_cast<int*>(post_empty + kPostRing);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ti_item + kTileRing);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   int* split_flag = last_flag + 1;
@@ -804,7 +808,16 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
   int* owner = dot_list + 64;       // [R]: commit group that last read each ring entry
   int* ti_kb = owner + R;           // [kTileRing]: balanced segment K range per ring slot
   int* bst = ti_kb + kTileRing;     // [3]: balanced scheduler state (stage, next, end)
+  int* post_req = bst + 4;          // [kPostRing]: item ids queued for the post warp
   const bool bal = p.balanced != 0;
+  // single-CTA kernels: the post warp takes the posts when a stage of this launch posts
+  // and the launch has at least four items per CTA (a short launch is latency-bound: the
+  // hand-off to another warp delays the consumer; measured +0.6-1 us at B <= 8)
+  bool any_post = false;
+  if constexpr (CG == 1) {
+    for (int s = 0; s < p.n_stages; ++s) any_post |= p.st[s].n_out_deps > 0;
+    any_post = any_post && p.item_hi - p.item_lo >= 4 * static_cast<int>(gridDim.x);
+  }
   const int unit = static_cast<int>(blockIdx.x) / (CG * NP);  // this CTA's work unit
   const int units = static_cast<int>(gridDim.x) / (CG * NP);  // all co-resident (host cap)
 
@@ -834,6 +847,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
     for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(&win_full[i], 1);
       ptx::mbar_init(&win_empty[i], 1);
+    }
+    for (int i = 0; i < kPostRing; ++i) {
+      ptx::mbar_init(&post_full[i], 1);
+      ptx::mbar_init(&post_empty[i], 1);
     }
     for (int i = 0; i < kTileRing; ++i) {
       ptx::mbar_init(&ti_full[i], 1);
@@ -1633,6 +1650,41 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         u += 1 + wide;
       }
     }
+  } else if (CG == 1 && warp == 3) {
+    // ===================== post warp (single-CTA kernels) =====================
+    // stage.post() of items the epilogue queued: the release fence waits for the tile's
+    // stores to be performed (~3k cycles after a 128-row store burst) — here, off the
+    // epilogue warps' per-item path. Ordering: the epilogue's stores, its named barrier,
+    // thread 128's arrive (release, CTA) -> this wait (acquire) -> the GPU-scope fence ->
+    // the release RMW on the consumer's semaphore.
+    if (lane == 0 && any_post) {
+#pragma unroll 1
+      for (int q = 0;; ++q) {
+        const int ps = q % kPostRing;
+        ptx::mbar_wait(&post_full[ps], (q / kPostRing) & 1);
+        const int g = post_req[ps];
+        ptx::mbar_arrive(&post_empty[ps]);
+        if (g < 0) break;
+        const Tile t = decode(p, g);
+        const StageParams& st = p.st[t.s];
+        __threadfence();
+        ptx::fence_proxy_async_global();
+        for (int i = 0; i < st.n_out_deps; ++i) {
+          const int d = st.out_deps[i];
+          const DepParams& dp = p.dep[d];
+          const int idx = post_target(dp.policy, dp.param, t.tx, t.ty,
+                                      Grid3{dp.pgx, dp.pgy, dp.pgz});
+          if (p.st[dp.consumer].kind == kStageAllReduce) {
+            __threadfence_system();
+            ptx::atom_add_release_sys(dp.sem + idx, 1);
+          } else {
+            ptx::red_add_release_gpu(dp.sem + idx, 1);
+          }
+          ptx::red_add_release_gpu(p.scratch + kDoneBase + d, 1);
+        }
+      }
+    }
+    __syncwarp();
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int ew = warp & 3;         // TMEM lanes [32*ew, 32*ew+32) (a warp's lane quarter)
@@ -1689,6 +1741,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
                                                   : ptx::policy_evict_last());
     };
     uint32_t local = 0;  // GeMM tiles (peer_done parity)
+    int npost = 0;       // single-CTA kernels: posts queued for the post warp (thread 128)
     uint32_t u = 0;      // TMEM accumulator-slot uses, as counted by the MMA warp
     uint32_t tmem_empty_remote[2] = {0, 0};
     if constexpr (CG == 2) {
@@ -2366,7 +2419,17 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       // stage.post(): every epilogue thread's stores (of both CTAs of a pair)
       // happen-before the release below.
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-      if (threadIdx.x == 128) {
+      // single-CTA kernels, untraced items without a last-arriver dot or row gate: the
+      // post warp makes the post (see above)
+      const bool apost = CG == 1 && any_post && p.trace == nullptr && st.dot_dep < 0 &&
+                         st.out_sem == nullptr && st.n_out_deps > 0 && brole != 1;
+      if (threadIdx.x == 128 && apost) {
+        const int ps = npost % kPostRing;
+        ptx::mbar_wait(&post_empty[ps], ((npost / kPostRing) & 1) ^ 1);
+        post_req[ps] = g;
+        ptx::mbar_arrive(&post_full[ps]);
+        ++npost;
+      } else if (threadIdx.x == 128) {
         if (CG == 2 && !uleader) {
           __threadfence();
           ptx::mbar_arrive_remote(ptx::mapa(&peer_done[local % kPeerRing], 0));
@@ -2473,6 +2536,12 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       }
       ++local;
       u += 1 + wide;
+    }
+    if (CG == 1 && threadIdx.x == 128 && any_post) {  // end of the post warp's queue
+      const int ps = npost % kPostRing;
+      ptx::mbar_wait(&post_empty[ps], ((npost / kPostRing) & 1) ^ 1);
+      post_req[ps] = -1;
+      ptx::mbar_arrive(&post_full[ps]);
     }
   }
 
