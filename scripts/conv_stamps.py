@@ -52,3 +52,8 @@ t0 = min(x for r in cta for x in r[:9] if x)
 print("CTA 5, items 0..9 (cycles from its first stamp):", " | ".join(names))
 for i in range(10):
     print(f"  {i:2d} " + " ".join(f"{(cta[i][k] - t0) if cta[i][k] else -1:8d}" for k in range(9)))
+# producer: claimed -> dependency waits done (slot 10, fused mode)
+w = [r[10] - r[7] for cta in raw for r in cta[2:38] if r[10] and r[7]]
+if w:
+    w = sorted(w)
+    print(f"  {'PROD: claimed -> dependency waits done':42s} {statistics.median(w):8.0f} {w[len(w)//10]:8.0f} {w[9*len(w)//10]:8.0f}")
