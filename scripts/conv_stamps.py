@@ -10,12 +10,14 @@ import paper_2305_13450_b200 as ts
 from paper_2305_13450_b200 import _lib
 hw, b = (int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "56:256").split(":"))
 mode = sys.argv[2] if len(sys.argv) > 2 else "stream"
-c = 64
+c = int(sys.argv[3]) if len(sys.argv) > 3 else 64
+tn = int(sys.argv[4]) if len(sys.argv) > 4 else 64
+halo = c == 64 and tn == 64
 torch.manual_seed(0)
 w1 = (torch.randn(c, 3, 3, c, device="cuda") / (9 * c) ** 0.5).half()
 w2 = (torch.randn(c, 3, 3, c, device="cuda") / (9 * c) ** 0.5).half()
 x = torch.randn(b, hw, hw, c, device="cuda").half()
-ch = ts.ConvChain(x, w1, w2, tile_n=64, cta_group=1, mode=mode, halo=True, extra_flags=1 << 7)
+ch = ts.ConvChain(x, w1, w2, tile_n=tn, cta_group=1, mode=mode, halo=halo, extra_flags=1 << 7)
 ch.cs.enable_trace(148 * 40 * 12 * 8 // _lib.TRACE_REC_BYTES + 64)
 for _ in range(3):
     ch()
@@ -42,7 +44,7 @@ rows = [("MMA: take -> window ready", d(0, 1)), ("MMA: window ready -> committed
         ("PROD: claimed -> window issued", d(7, 8)), ("PROD: window issued -> next claim", dn(7, 8)),
         ("item period (MMA take -> next take)", dn(0, 0)), ("item period (EPI end -> next end)", dn(6, 6)),
         ("MMA commit -> EPI acc ready", [r[4] - r[2] for cta in raw for r in cta[2:38] if r[4] and r[2]])]
-print(f"halo conv {hw}x{hw}x64 B={b} {mode}: per-item phases, cycles (median / p10 / p90 over CTAs x items 2..37)")
+print(f"conv {hw}x{hw}x{c} tile_n {tn} halo {halo} B={b} {mode}: per-item phases, cycles (median / p10 / p90 over CTAs x items 2..37)")
 for name, v in rows:
     if v:
         v = sorted(v)
@@ -57,3 +59,7 @@ w = [r[10] - r[7] for cta in raw for r in cta[2:38] if r[10] and r[7]]
 if w:
     w = sorted(w)
     print(f"  {'PROD: claimed -> dependency waits done':42s} {statistics.median(w):8.0f} {w[len(w)//10]:8.0f} {w[9*len(w)//10]:8.0f}")
+w = [r[11] - r[1] for cta in raw for r in cta[2:38] if r[11] and r[1]]
+if w:
+    w = sorted(w)
+    print(f"  {'MMA: first K-block (operand wait)':42s} {statistics.median(w):8.0f} {w[len(w)//10]:8.0f} {w[9*len(w)//10]:8.0f}")
