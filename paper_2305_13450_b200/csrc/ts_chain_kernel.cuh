@@ -278,6 +278,15 @@ __device__ __forceinline__ void trace_event(const ChainParams& p, uint64_t t, in
   p.trace[slot] = r;
 }
 
+// trace_event stamped now. The timer is read only when tracing: %globaltimer is an
+// `asm volatile` read the compiler keeps even when trace_event returns at once, and two of
+// them per consumer wait cost a fused conv pair ~8% (r02s3).
+template <typename... A>
+__device__ __forceinline__ void trace_now(const ChainParams& p, A... a) {
+  if (p.trace == nullptr) return;
+  trace_event(p, ptx::global_timer(), a...);
+}
+
 template <typename T>
 struct AbFormat;
 template <>
@@ -1035,7 +1044,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         const Tile t = decode(p, g);
         const StageParams& st = p.st[t.s];
         if (uleader)
-          trace_event(p, ptx::global_timer(), 0, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
+          trace_now(p, 0, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
         if (st.kind == kStageDot || st.kind == kStageAllReduce)
           continue;  // pointwise stages: the epilogue warps run them
         if constexpr (C::kHaloOk) {
@@ -1059,7 +1068,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
             if (d >= 0 && !((p.flags >> 12) & 1)) {
               const DepParams& dp = p.dep[d];
               if (uleader)
-                trace_event(p, ptx::global_timer(), 1, t.s, t.tb, 0, d, t.tx, dp.pgz, t.tx, t.ty, t.tz);
+                trace_now(p, 1, t.s, t.tb, 0, d, t.tx, dp.pgz, t.tx, t.ty, t.tz);
               const int base_t = ht.n * st.htpi;
               auto wait_tile = [&](int u) {
                 if (!((done_mask >> d) & 1) &&
@@ -1081,7 +1090,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
                   for (int sg = s0; sg <= s1; ++sg) wait_tile(base_t + rg * st.htpr + sg);
               }
               if (uleader)
-                trace_event(p, ptx::global_timer(), 2, t.s, t.tb, 0, d, t.tx, dp.pgz, t.tx, t.ty, t.tz);
+                trace_now(p, 2, t.s, t.tb, 0, d, t.tx, dp.pgz, t.tx, t.ty, t.tz);
               ptx::fence_proxy_async_global();
             }
             // (3) the window: input rows h0 - 1 .. h0 + hrows - 2 (+ halo columns), once
@@ -1120,10 +1129,14 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         auto wait_kstep = [&](int ks) {
           const DepParams& dp = p.dep[d];
           const Grid3 pg{dp.pgx, dp.pgy, dp.pgz};
+          // the producer-done watermark was observed (and fenced) earlier in this launch:
+          // every wait of d is satisfied, and the fence after that observation orders all
+          // later TMA reads of this thread (traced launches still record the wait events)
+          if (((done_mask >> d) & 1) && p.trace == nullptr) return;
           Wait w = consumer_wait(dp.policy, dp.param, t.tx, t.ty, ks, pg, dp.pgz);
           if (w.sem < 0) return;
           if (uleader)
-            trace_event(p, ptx::global_timer(), 1, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
+            trace_now(p, 1, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
                         t.ty, t.tz);
           // Halo (extension): a 3x3 window of output rows [m0, m0 + tile_m) reads input
           // pixels up to W + 1 rows away, i.e. the same k-step's producer tiles of
@@ -1148,7 +1161,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
                    sem_wait_dep(p, d, dp.sem + w.sem, w.expected, h1, e1, h2, e2, h3, e3, h4, e4))
             done_mask |= 1u << d;
           if (uleader)
-            trace_event(p, ptx::global_timer(), 2, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
+            trace_now(p, 2, t.s, t.tb, ks, d, w.sem, w.expected, t.tx,
                         t.ty, t.tz);
           ptx::fence_proxy_async_global();
         };
@@ -1474,7 +1487,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
               // in the single issuing thread, on the per-item critical path)
               if (tr) {
                 const Tile t5 = decode(p, g);
-                trace_event(p, ptx::global_timer(), 5, t5.s, t5.tb, -1, -1, -1, -1, t5.tx, t5.ty);
+                trace_now(p, 5, t5.s, t5.tb, -1, -1, -1, -1, t5.tx, t5.ty);
               }
               // tap (r, s): A = the window from row r * hs + s (16-B descriptor units: 8 per
               // 128-B row), B = tap weights (8 KB = 512 units apart)
@@ -1527,7 +1540,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
           }
           if (tr && kb == 0 && lane == 0) {
             const Tile t = decode(p, g);
-            trace_event(p, ptx::global_timer(), 5, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty);
+            trace_now(p, 5, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty);
           }
           ptx::tc_fence_after();
           if (lane == 0) {
@@ -1641,7 +1654,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
           }
           if (tr) {
             const Tile t = decode(p, g);
-            trace_event(p, ptx::global_timer(), 6, t.s, t.tb, -1, -1, -1,
+            trace_now(p, 6, t.s, t.tb, -1, -1, -1,
                         static_cast<int>(starve_ns > 0x7fffffff ? 0x7fffffff : starve_ns), t.tx,
                         t.ty);
           }
@@ -1758,7 +1771,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
       ptx::fence_acq_rel_gpu();
       if (threadIdx.x == 128 && half <= 0)
-        trace_event(p, ptx::global_timer(), 7, ds, tb, -1, -1, -1, -1, tx, ty);
+        trace_now(p, 7, ds, tb, -1, -1, -1, -1, tx, ty);
       // a dot tile covers BN / 128 heads (the paper's stride H / (8 Ty));
       // one warp per (row, head), warps striding over the tile's rows x heads
       constexpr int kHeads = BN >= 128 ? BN / 128 : 1;
@@ -1774,7 +1787,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
     auto post_dot = [&](int ds, int tx, int ty, int tb) {
       const StageParams& sd = p.st[ds];
       if (threadIdx.x == 128) {
-        const uint64_t tnow = ptx::global_timer();
+        const uint64_t tnow = p.trace ? ptx::global_timer() : 0;  // traced launches only
         trace_event(p, tnow, 8, ds, tb, -1, -1, -1, -1, tx, ty);
         __threadfence();
         ptx::fence_proxy_async_global();
@@ -1846,10 +1859,10 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
           Wait w = consumer_wait(dp.policy, dp.param, t.tx, t.ty, 0, Grid3{dp.pgx, dp.pgy, dp.pgz},
                                  dp.pgz);
           if (w.sem >= 0) {
-            trace_event(p, ptx::global_timer(), 1, t.s, t.tb, 0, st.in_dep, w.sem, w.expected,
+            trace_now(p, 1, t.s, t.tb, 0, st.in_dep, w.sem, w.expected,
                         t.tx, t.ty, t.tz);
             sem_wait(p, dp.sem + w.sem, w.expected);
-            trace_event(p, ptx::global_timer(), 2, t.s, t.tb, 0, st.in_dep, w.sem, w.expected,
+            trace_now(p, 2, t.s, t.tb, 0, st.in_dep, w.sem, w.expected,
                         t.tx, t.ty, t.tz);
           }
         }
@@ -1862,7 +1875,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         ptx::mbar_wait(&tmem_full[(u + j) & 1], ((u + j) >> 1) & 1);
       ptx::tc_fence_after();
       if (threadIdx.x == 128 && uleader && p.trace != nullptr)  // epilogue begin (extension)
-        trace_event(p, ptx::global_timer(), 7, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
+        trace_now(p, 7, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
       const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
       const uint32_t t_lane = lane_base + (u & 1) * C::kAccCols;
       // accumulator column x of this tile (a double-width tile spans both slots)
@@ -2083,7 +2096,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
           asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
           if (threadIdx.x == 128) {
             if (uleader && p.trace != nullptr)  // partial written (extension)
-              trace_event(p, ptx::global_timer(), 9, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
+              trace_now(p, 9, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
             ptx::fence_proxy_async_global();  // the owner reads the plane with TMA
             ptx::atom_add_release_gpu(rdy, 1);
           }
@@ -2222,7 +2235,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         __threadfence();
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
         if (threadIdx.x == 128 && uleader && p.trace != nullptr)  // partials written (ext.)
-          trace_event(p, ptx::global_timer(), 9, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
+          trace_now(p, 9, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
         if (threadIdx.x == 128) {
           const int half_id = tile_id * CG * NP + static_cast<int>(qrank);
           const int old = atomicAdd(&st.cnt[half_id], 1);
@@ -2415,7 +2428,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
       }
       }  // normal layout
       if (threadIdx.x == 128 && uleader && p.trace != nullptr)  // epilogue stores issued
-        trace_event(p, ptx::global_timer(), 8, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
+        trace_now(p, 8, t.s, t.tb, -1, -1, -1, -1, t.tx, t.ty, t.tz);
       // stage.post(): every epilogue thread's stores (of both CTAs of a pair)
       // happen-before the release below.
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
@@ -2436,7 +2449,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
         } else {
           if constexpr (CG == 2)
             ptx::mbar_wait_cluster(&peer_done[local % kPeerRing], (local / kPeerRing) & 1);
-          const uint64_t tnow = ptx::global_timer();
+          const uint64_t tnow = p.trace ? ptx::global_timer() : 0;  // traced launches only
           // a balanced segment that does not start its tile only contributed a partial:
           // the tile is posted once, by its head segment after the reduction
           const bool posts = brole != 1;
@@ -2469,7 +2482,7 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
                 // (x, c) at k-step 0 is on semaphore idx and now reached its threshold)
                 const StageParams& sd = p.st[dp.consumer];
                 // time read after the atomic: later than every post it counted
-                const uint64_t tfire = ptx::global_timer();
+                const uint64_t tfire = p.trace ? ptx::global_timer() : 0;
                 int n = 0;
                 for (int c = 0; c < sd.grid_y; ++c) {
                   Wait w = consumer_wait(dp.policy, dp.param, t.tx, c, 0,
