@@ -259,8 +259,12 @@ def main():
         base, bcands = planner.pick_mlp(x, w1, w2, mode="stream")
         if b == 1024:
             # guard against a noisy pick: the planner's choice and the fixed plan are
-            # re-timed round robin (3 x 20 chains each) and the faster median is kept
-            best = planner.pick_between(x, w1, w2, [best, dict(fixed, mode="fused")])
+            # re-timed round robin under sustained load (4 x 200 chains each: the power cap
+            # settles over ~100 ms, and short bursts favour the split plans whose extra
+            # DRAM traffic costs clock later; profiles/r02s3e_sustained.txt) and the faster
+            # median is kept, the fixed plan on ties
+            best = planner.pick_between(x, w1, w2, [dict(fixed, mode="fused"), best],
+                                        rounds=4, iters=200)
     else:
         best, cands = dict(fixed, mode="fused"), []
         base, bcands = dict(fixed, mode="stream"), []
