@@ -28,6 +28,10 @@ plans = {
     "stream z1 RowMajor": dict(base, mode="stream"),
     "stream z2 Band4": dict(base, mode="stream", prod_splits=2,
                             cons_order=ts.BandedColumnMajor(4)),
+    "stream z1 Band3 tail22x2": dict(base, mode="stream", cons_order=ts.BandedColumnMajor(3),
+                                     cons_tail=(22, 2)),
+    "stream z1 Band4 tail22x2": dict(base, mode="stream", cons_order=ts.BandedColumnMajor(4),
+                                     cons_tail=(22, 2)),
 }
 chains = {k: ts.MlpChain(x, w1, w2, **kw) for k, kw in plans.items()}
 
