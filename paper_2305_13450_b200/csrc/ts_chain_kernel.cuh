@@ -1070,24 +1070,28 @@ __global__ void __launch_bounds__(Cfg<BN, CG, SW, QD>::kThreads, 1)
               if (uleader)
                 trace_now(p, 1, t.s, t.tb, 0, d, t.tx, dp.pgz, t.tx, t.ty, t.tz);
               const int base_t = ht.n * st.htpi;
-              auto wait_tile = [&](int u) {
-                if (!((done_mask >> d) & 1) &&
-                    sem_wait_dep(p, d, dp.sem + u, dp.pgz, nullptr, 0, nullptr, 0, nullptr, 0,
-                                 nullptr, 0))
-                  done_mask |= 1u << d;
+              // producer tiles [u, u + n) (contiguous semaphores), probed five at a time in
+              // one round trip (one sem_wait_dep per tile serialized 2-6 loaded-L2 round
+              // trips per item until the producer-done watermark was seen)
+              auto wait_range = [&](int u, int n) {
+                for (; n > 0 && !((done_mask >> d) & 1); u += 5, n -= 5) {
+                  const int* s0 = dp.sem + u;
+                  if (sem_wait_dep(p, d, s0, dp.pgz, n > 1 ? s0 + 1 : nullptr, dp.pgz,
+                                   n > 2 ? s0 + 2 : nullptr, dp.pgz, n > 3 ? s0 + 3 : nullptr,
+                                   dp.pgz, n > 4 ? s0 + 4 : nullptr, dp.pgz))
+                    done_mask |= 1u << d;
+                }
               };
               const int hlo = ht.h0 > 0 ? ht.h0 - 1 : 0;
+              const int hhi0 = ht.h0 + st.hrpt;  // last input row the window reads
+              const int hhi = hhi0 < st.conv_h - 1 ? hhi0 : st.conv_h - 1;
               if (st.hmode == 1) {
-                const int hhi0 = ht.h0 + st.hrpt;  // last input row the window reads
-                const int hhi = hhi0 < st.conv_h - 1 ? hhi0 : st.conv_h - 1;
-                for (int u = hlo / st.hrpt; u <= hhi / st.hrpt; ++u) wait_tile(base_t + u);
+                wait_range(base_t + hlo / st.hrpt, hhi / st.hrpt - hlo / st.hrpt + 1);
               } else {
-                const int hhi0 = ht.h0 + st.hrpt;  // last input row the window reads
-                const int hhi = hhi0 < st.conv_h - 1 ? hhi0 : st.conv_h - 1;
                 const int s0 = ht.w0 > 0 ? (ht.w0 - 1) / 128 : 0;
                 const int s1 = (ht.w0 + 128 < st.conv_w - 1 ? ht.w0 + 128 : st.conv_w - 1) / 128;
                 for (int rg = hlo / st.hrpt; rg <= hhi / st.hrpt; ++rg)
-                  for (int sg = s0; sg <= s1; ++sg) wait_tile(base_t + rg * st.htpr + sg);
+                  wait_range(base_t + rg * st.htpr + s0, s1 - s0 + 1);
               }
               if (uleader)
                 trace_now(p, 2, t.s, t.tb, 0, d, t.tx, dp.pgz, t.tx, t.ty, t.tz);
